@@ -1,0 +1,328 @@
+"""Public API — factorize / solve / logdet / factorize_many (the SPEC api
+surface, which the reference snapshot does not ship).
+
+Pipeline: structure stats -> ordering policy -> permute ->
+tile symbolic (C++) -> device launch plan (cached per pattern) -> H2D of the
+permuted CSC values -> device scatter into tile storage -> CUDA-graph
+factorisation with fused log-determinant.  Everything numeric runs on the GPU.
+Problems sharing a sparsity pattern share one ordering, symbolic analysis,
+plan and scatter map (the INLA batch case).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import time
+from collections import OrderedDict
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .ctsf import TiledMatrix, build_tile_grid
+from .errors import FactorizeManyError, NotPositiveDefiniteError
+from .matcore import SymmetricCsc, permute_symmetric, structure_stats
+from .ordering import (FillReport, Permutation, adaptable_nd, min_degree, rcm,
+                       select_ordering, symbolic_fill_count)
+from .scheduler import DevicePlan, PlanOptions
+from .symbolic import TileSymbolic, tile_symbolic_factorize
+
+__all__ = ["FactorOptions", "FactorContext", "factorize", "solve", "logdet", "factorize_many",
+           "factorize_many_sharded", "clear_plan_cache"]
+
+_ORDERINGS = ("auto", "identity", "partial-rcm", "min-degree", "adaptable-nd")
+_REDUCTIONS = ("auto", "on", "off")
+
+
+@dataclass(frozen=True)
+class FactorOptions:
+    """SPEC.md:482-485 options plus B200 plan knobs.
+
+    ``workers`` keeps its reference meaning for the tree-reduction rule
+    (chains >= 2*workers are split); with workers < 2 the device default of 8
+    partial accumulators is used."""
+
+    tile_size: int = 120
+    workers: int = 1
+    ordering: str = "auto"
+    tree_reduction: str = "auto"
+    lookahead: bool = True
+    use_graph: bool = True
+    chunk: int = 0
+
+    def __post_init__(self):
+        if self.tile_size < 1:
+            raise ValueError(f"tile_size must be >= 1, got {self.tile_size}")
+        if self.workers < 1:
+            raise ValueError(f"workers must be >= 1, got {self.workers}")
+        if self.ordering not in _ORDERINGS:
+            raise ValueError(f"unknown ordering policy {self.ordering!r}")
+        if self.tree_reduction not in _REDUCTIONS:
+            raise ValueError(f"unknown tree_reduction policy {self.tree_reduction!r}")
+
+    def plan_options(self) -> PlanOptions:
+        W = self.workers if self.workers >= 2 else 8
+        thr = -1 if self.tree_reduction == "off" else 0
+        return PlanOptions(tree_workers=min(W, 16), tree_threshold=thr, chunk=self.chunk,
+                           lookahead=self.lookahead, use_graph=self.use_graph)
+
+
+@dataclass(eq=False)
+class FactorContext:
+    """Result of factorize: permutation, device factor,
+    symbolic structure, stats.  Immutable after creation."""
+
+    permutation: Permutation
+    factor: TiledMatrix
+    symbolic: TileSymbolic
+    stats: dict = field(default_factory=dict)
+    plan: DevicePlan | None = None
+    _logdet: float = float("nan")
+
+    @property
+    def n(self) -> int:
+        return self.factor.grid.n
+
+
+# ---------------------------------------------------------------- caching --
+class _Pattern:
+    """Everything that depends only on (pattern, options)."""
+
+    def __init__(self, m: SymmetricCsc, opts: FactorOptions):
+        t0 = time.perf_counter()
+        self.stats = structure_stats(m)
+        self.perm = _choose_ordering(m, opts, self.stats)
+        t1 = time.perf_counter()
+        if self.perm.is_identity():
+            self.pm_pattern = m
+            self.gather = None
+        else:
+            # permuted pattern + the value gather it implies (values are moved,
+            # never combined, since permute_symmetric rejects duplicates)
+            probe = SymmetricCsc(m.n, m.col_ptr, m.row_idx, np.arange(m.nnz, dtype=np.float64))
+            pp = permute_symmetric(probe, self.perm)
+            self.gather = pp.values.astype(np.int64)
+            self.pm_pattern = SymmetricCsc(m.n, pp.col_ptr, pp.row_idx, pp.values)
+        t2 = time.perf_counter()
+        grid = build_tile_grid(self.pm_pattern, opts.tile_size)
+        self.symbolic = tile_symbolic_factorize(grid)
+        t3 = time.perf_counter()
+        self.plan = _get_plan(self.symbolic, opts.plan_options())
+        self.offsets_dev = None
+        t4 = time.perf_counter()
+        self.times = {"ordering_s": t1 - t0, "permute_s": t2 - t1, "symbolic_s": t3 - t2,
+                      "plan_s": t4 - t3}
+        self.fill = None
+
+    def offsets(self):
+        if self.offsets_dev is None:
+            import torch
+            off = self.plan.offsets_for(self.pm_pattern)
+            self.offsets_dev = torch.from_numpy(off).cuda()
+        return self.offsets_dev
+
+    def permuted_values(self, m: SymmetricCsc) -> np.ndarray:
+        return m.values if self.gather is None else m.values[self.gather]
+
+
+_PLANS: "OrderedDict[tuple, DevicePlan]" = OrderedDict()
+_PATTERNS: "OrderedDict[tuple, _Pattern]" = OrderedDict()
+_MAX_CACHE = 8
+
+
+def clear_plan_cache() -> None:
+    _PLANS.clear()
+    _PATTERNS.clear()
+
+
+def _lru(cache, key, make):
+    if key in cache:
+        cache.move_to_end(key)
+        return cache[key]
+    val = make()
+    cache[key] = val
+    while len(cache) > _MAX_CACHE:
+        cache.popitem(last=False)
+    return val
+
+
+def _get_plan(sym: TileSymbolic, popts: PlanOptions) -> DevicePlan:
+    fg = sym.factor_grid
+    h = hashlib.sha1(fg.keys.tobytes()).hexdigest()
+    return _lru(_PLANS, (fg.n, fg.nt, h, popts), lambda: DevicePlan(fg, popts))
+
+
+def _pattern_for(m: SymmetricCsc, opts: FactorOptions) -> _Pattern:
+    h = hashlib.sha1()
+    h.update(np.ascontiguousarray(m.col_ptr).tobytes())
+    h.update(np.ascontiguousarray(m.row_idx).tobytes())
+    key = (m.n, h.hexdigest(), opts.tile_size, opts.ordering, opts.plan_options())
+    return _lru(_PATTERNS, key, lambda: _Pattern(m, opts))
+
+
+def _choose_ordering(m: SymmetricCsc, opts: FactorOptions, stats) -> Permutation:
+    pol = opts.ordering
+    if pol == "identity":
+        return Permutation.identity(m.n)
+    if pol == "partial-rcm":
+        return rcm(m, pinned_tail=stats.thickness)
+    if pol == "min-degree":
+        return min_degree(m)
+    if pol == "adaptable-nd":
+        return adaptable_nd(m, stats)
+    return select_ordering(m, [rcm(m, pinned_tail=stats.thickness), adaptable_nd(m, stats)])
+
+
+# ------------------------------------------------------------- factorize --
+def _stream_handle(stream) -> int:
+    return stream.cuda_stream
+
+
+def _launch(pat: _Pattern, m: SymmetricCsc, lane: int, stream, storage=None):
+    """H2D values, device scatter, async factorisation on `stream`."""
+    import torch
+    vals = np.ascontiguousarray(pat.permuted_values(m), dtype=np.float64)
+    host = torch.from_numpy(vals).pin_memory() if vals.nbytes > (1 << 20) else torch.from_numpy(vals)
+    with torch.cuda.stream(stream):
+        dev = host.to("cuda", non_blocking=True)
+        if storage is None:
+            storage = pat.plan.new_storage()
+        pat.plan.pack(dev, pat.offsets(), storage, _stream_handle(stream))
+        pat.plan.factorize_async(storage, lane, _stream_handle(stream))
+    return storage, (host, dev)
+
+
+def _finish(pat: _Pattern, m: SymmetricCsc, storage, lane: int, stream, t_start=None) -> FactorContext:
+    fail, ld = pat.plan.collect(lane, _stream_handle(stream))
+    if fail >= 0:
+        idx = int(fail)
+        orig = int(pat.perm.inverse[idx]) if idx < m.n else None
+        raise NotPositiveDefiniteError(idx, orig)
+    if pat.fill is None:
+        pat.fill = symbolic_fill_count(pat.pm_pattern) if m.n <= 2_000_000 else None
+    stats = dict(pat.times)
+    stats["fill"] = pat.fill
+    stats["tile_flops"] = pat.plan.info()["tile_flops"]
+    if t_start is not None:
+        stats["numeric_wall_s"] = time.perf_counter() - t_start
+    fac = TiledMatrix(grid=pat.symbolic.factor_grid, storage=storage)
+    return FactorContext(permutation=pat.perm, factor=fac, symbolic=pat.symbolic, stats=stats,
+                         plan=pat.plan, _logdet=ld)
+
+
+def factorize(m: SymmetricCsc, opts: FactorOptions | None = None) -> FactorContext:
+    """Order, analyse, plan and factorise ``m`` on the current CUDA device."""
+    import torch
+    _lib.require_device()
+    opts = opts or FactorOptions()
+    pat = _pattern_for(m, opts)
+    stream = torch.cuda.current_stream()
+    t0 = time.perf_counter()
+    storage, _keep = _launch(pat, m, 0, stream)
+    return _finish(pat, m, storage, 0, stream, t0)
+
+
+def logdet(ctx: FactorContext) -> float:
+    """2 * sum log diag(L) over non-padding entries; fused
+    into the factorisation graph, recomputed on device when unavailable."""
+    if np.isfinite(ctx._logdet):
+        return float(ctx._logdet)
+    return ctx.plan.logdet(ctx.factor.storage)
+
+
+def solve(ctx: FactorContext, rhs) -> np.ndarray:
+    """x with A x = b via permuted tile forward/back substitution on the GPU
+    (SPEC.md:499-505).  rhs: (n,) or (n, k)."""
+    import torch
+    b = np.asarray(rhs, dtype=np.float64)
+    n = ctx.n
+    if b.shape[0] != n or b.ndim not in (1, 2):
+        raise ValueError(f"rhs length {b.shape[0]} does not match order {n}")
+    cols = b.reshape(n, -1)
+    k = cols.shape[1]
+    T, nt = ctx.plan.T, ctx.plan.nt
+    y = np.zeros((k, T * nt))
+    y[:, :n] = cols[ctx.permutation.inverse].T
+    dev = torch.from_numpy(y).cuda()
+    ctx.plan.solve(ctx.factor.storage, dev)
+    x = dev.cpu().numpy()[:, :n][:, ctx.permutation.forward].T
+    return x.reshape(b.shape).copy()
+
+
+def factorize_many(problems, opts: FactorOptions | None = None, lanes: int = 4) -> list:
+    """Independent factorisations run concurrently on `lanes` CUDA streams of
+    the current device.  ``problems``: list of matrices or
+    (matrix, options) pairs.  Results are bitwise those of solo runs; failures
+    are aggregated into FactorizeManyError without cancelling siblings."""
+    import torch
+    _lib.require_device()
+    items = [(p, opts or FactorOptions()) if isinstance(p, SymmetricCsc) else (p[0], p[1] or opts or FactorOptions())
+             for p in problems]
+    streams = [torch.cuda.Stream() for _ in range(max(1, lanes))]
+    results: list = [None] * len(items)
+    errors: dict = {}
+    pending = []
+    for i, (m, o) in enumerate(items):
+        lane = i % len(streams)
+        if len(pending) >= len(streams):
+            _drain(pending.pop(0), results, errors)
+        try:
+            pat = _pattern_for(m, o)
+            storage, keep = _launch(pat, m, lane, streams[lane])
+            pending.append((i, pat, m, storage, lane, streams[lane], keep))
+        except Exception as e:  # noqa: BLE001 - per-problem aggregation
+            errors[i] = e
+    while pending:
+        _drain(pending.pop(0), results, errors)
+    if errors:
+        raise FactorizeManyError(errors, results)
+    return results
+
+
+def _drain(entry, results, errors):
+    i, pat, m, storage, lane, stream, _keep = entry
+    try:
+        results[i] = _finish(pat, m, storage, lane, stream)
+    except Exception as e:  # noqa: BLE001
+        errors[i] = e
+
+
+def factorize_many_sharded(problems, rhs=None, opts: FactorOptions | None = None, lanes: int = 4,
+                           group=None, return_solutions: bool = True):
+    """Batch factorisation sharded over the ranks of a torch.distributed
+    (NCCL) group: rank r takes the contiguous block of problems
+    [r*P/W, (r+1)*P/W).  Only per-problem log-determinants (and solutions of
+    ``rhs`` when given) are exchanged — one all-gather over NVLink.
+
+    Returns {"logdet": float64[P], "x": list of arrays or None, "local": local results}."""
+    import torch
+    import torch.distributed as dist
+    P = len(problems)
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    lo, hi = (rank * P) // world, ((rank + 1) * P) // world
+    local = factorize_many(problems[lo:hi], opts=opts, lanes=lanes) if hi > lo else []
+    n = problems[0].n if isinstance(problems[0], SymmetricCsc) else problems[0][0].n
+    per = (hi - lo)
+    width = 1 + (n if (rhs is not None and return_solutions) else 0)
+    cap = -(-P // world)
+    buf = torch.zeros((cap, width), dtype=torch.float64, device="cuda")
+    for j, ctx in enumerate(local):
+        buf[j, 0] = logdet(ctx)
+        if width > 1:
+            b = rhs[lo + j] if isinstance(rhs, (list, tuple)) else rhs
+            buf[j, 1:] = torch.from_numpy(solve(ctx, b)).cuda()
+    if world > 1:
+        out = [torch.empty_like(buf) for _ in range(world)]
+        dist.all_gather(out, buf, group=group)
+    else:
+        out = [buf]
+    gathered = []
+    for r in range(world):
+        a, b = (r * P) // world, ((r + 1) * P) // world
+        gathered.append(out[r][: b - a])
+    allv = torch.cat(gathered).cpu().numpy()
+    del per
+    return {"logdet": allv[:, 0].copy(),
+            "x": [allv[i, 1:].copy() for i in range(P)] if width > 1 else None,
+            "local": local}

@@ -1,0 +1,1163 @@
+// tc_device.cu — C ABI of the device path: single-tile kernels, the
+// run_ops / replay_residual plugin entries and the optimised launch plan.
+// See include/tilechol_b200.h for the contract of every entry point.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "tc_kernels.cuh"
+#include "tilechol_b200.h"
+
+using namespace tc;
+
+// ---------------------------------------------------------------- errors --
+static thread_local std::string g_err;
+
+static int set_err(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return set_err(TC_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,       \
+                           cudaGetErrorString(e_));                                       \
+    } while (0)
+
+extern "C" const char* tc_last_error(void) { return g_err.c_str(); }
+extern "C" int32_t tc_abi_version(void) { return 1; }
+extern "C" int32_t tc_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+// ----------------------------------------------------- kernel selection --
+namespace {
+
+struct UpdKernel {
+    void (*fn)(UpdArgs);
+    int BM, BN, nth, smem;
+};
+
+template <int BM, int BN, int WGM, int WGN, int KS>
+UpdKernel mk_upd() {
+    using C = UpdCfg<BM, BN, WGM, WGN, KS>;
+    return UpdKernel{k_update<BM, BN, WGM, WGN, KS>, BM, BN, C::NTH, C::SMEM};
+}
+
+// Block shape per tile size: blocks that divide nt exactly where possible so
+// no MMA work is wasted on padding (120 -> 40x40, 160/320 -> 80x40,
+// 240/480 -> 80x48), small / odd sizes fall back to predicated 32x32.
+UpdKernel pick_upd(int nt) {
+    if (nt % 80 == 0 && nt % 48 == 0) return mk_upd<80, 48, 2, 2, 1>();
+    if (nt % 80 == 0) return mk_upd<80, 40, 2, 1, 2>();
+    if (nt % 40 == 0) return mk_upd<40, 40, 1, 1, 4>();
+    if (nt >= 96) return mk_upd<64, 64, 2, 2, 1>();
+    return mk_upd<32, 32, 2, 2, 1>();
+}
+
+int prep_kernel(const void* fn, int smem) {
+    if (smem > 48 * 1024) {
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    }
+    return TC_OK;
+}
+
+size_t potrf_smem(int nt, bool* in_smem) {
+    const int ntp = (nt + 7) & ~7;
+    if (ntp <= 160) {
+        *in_smem = true;
+        return (size_t)ntp * pad_ld(ntp) * 8 + (size_t)ntp * 8;
+    }
+    *in_smem = false;
+    return (size_t)ntp * 8;
+}
+
+bool potrf_supported(int nt) {
+    const int ntp = (nt + 7) & ~7;
+    return ntp <= 160 || nt % 8 == 0;
+}
+
+constexpr int kMaxTrsmNt = 480;
+
+inline double* tptr(double* st, double* sc, int64_t S, int64_t s, int nt) {
+    const size_t nt2 = (size_t)nt * nt;
+    return s < S ? st + (size_t)s * nt2 : sc + (size_t)(s - S) * nt2;
+}
+
+int launch_update_single(const UpdKernel& K, double* st, double* sc, int64_t S, int nt, int64_t dst,
+                         int64_t a, int64_t b, const int64_t* fail, cudaStream_t s) {
+    int r = prep_kernel((const void*)K.fn, K.smem);
+    if (r) return r;
+    UpdArgs ua{};
+    ua.storage = st;
+    ua.scratch = sc;
+    ua.S = S;
+    ua.fail = fail;
+    ua.nt = nt;
+    ua.s_dst = (int32_t)dst;
+    ua.s_a = (int32_t)a;
+    ua.s_b = (int32_t)b;
+    ua.s_mode = MODE_SUB;
+    const int nrb = (nt + K.BM - 1) / K.BM, ncb = (nt + K.BN - 1) / K.BN;
+    K.fn<<<nrb * ncb, K.nth, K.smem, s>>>(ua);
+    CK(cudaGetLastError());
+    return TC_OK;
+}
+
+int launch_potrf_direct(double* tile, int nt, int32_t* info_dev, const int64_t* fail, int64_t op_index,
+                        int64_t* fail_p, int32_t* fail_info, cudaStream_t s) {
+    if (!potrf_supported(nt))
+        return set_err(TC_ERR_ARG, "potrf: nt=%d > 160 must be a multiple of 8", nt);
+    bool in_smem;
+    const size_t sm = potrf_smem(nt, &in_smem);
+    int r = prep_kernel((const void*)k_potrf, (int)sm);
+    if (r) return r;
+    PotrfArgs pa{};
+    pa.tile = tile;
+    pa.info_out = info_dev;
+    pa.nt = nt;
+    pa.in_smem = in_smem;
+    pa.fail = fail;
+    pa.op_index = op_index;
+    pa.fail_p = fail_p;
+    pa.fail_info = fail_info;
+    k_potrf<<<1, kPotrfThreads, sm, s>>>(pa);
+    CK(cudaGetLastError());
+    return TC_OK;
+}
+
+int launch_trsm_direct(const double* L, double* X, int nt, int32_t* info_dev, const int64_t* fail, int64_t op_index,
+                       int64_t* fail_p, int32_t* fail_info, cudaStream_t s) {
+    if (nt > kMaxTrsmNt) return set_err(TC_ERR_ARG, "trsm: nt=%d > %d unsupported", nt, kMaxTrsmNt);
+    const size_t sm = trsm_smem_bytes(nt);
+    int r = prep_kernel((const void*)k_trsm, (int)sm);
+    if (r) return r;
+    TrsmArgs ta{};
+    ta.L = L;
+    ta.X = X;
+    ta.nt = nt;
+    ta.fail = fail;
+    ta.check_zero = 1;
+    ta.info_out = info_dev;
+    ta.op_index = op_index;
+    ta.fail_p = fail_p;
+    ta.fail_info = fail_info;
+    dim3 grid((nt + kTrsmRows - 1) / kTrsmRows, 1);
+    k_trsm<<<grid, kTrsmThreads, sm, s>>>(ta);
+    CK(cudaGetLastError());
+    return TC_OK;
+}
+
+int elem_grid(int nt) {
+    const size_t n2 = (size_t)nt * nt;
+    return (int)std::min<size_t>((n2 + 255) / 256, 592);
+}
+
+// small device scratch for status words of synchronous entry points
+struct StatusBuf {
+    int64_t* fail_p = nullptr;
+    int32_t* info = nullptr;
+    int alloc(cudaStream_t s) {
+        void* p = nullptr;
+        CK(cudaMallocAsync(&p, 16, s));
+        fail_p = (int64_t*)p;
+        info = (int32_t*)((char*)p + 8);
+        const int64_t init[2] = {kNoFail, (int64_t)-1};
+        CK(cudaMemcpyAsync(p, init, 16, cudaMemcpyHostToDevice, s));
+        return TC_OK;
+    }
+    void release(cudaStream_t s) {
+        if (fail_p) cudaFreeAsync(fail_p, s);
+        fail_p = nullptr;
+    }
+};
+
+}  // namespace
+
+// ------------------------------------------------------ tile entry points --
+extern "C" int tc_potrf_tile(double* a, int32_t nt, void* stream, int32_t* info) {
+    if (!a || nt < 1 || !info) return set_err(TC_ERR_ARG, "potrf_tile: bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    StatusBuf sb;
+    int r = sb.alloc(s);
+    if (r) return r;
+    r = launch_potrf_direct(a, nt, sb.info, nullptr, 0, nullptr, nullptr, s);
+    if (r) return r;
+    CK(cudaMemcpyAsync(info, sb.info, 4, cudaMemcpyDeviceToHost, s));
+    sb.release(s);
+    CK(cudaStreamSynchronize(s));
+    return TC_OK;
+}
+
+extern "C" int tc_trsm_tile(const double* l, double* x, int32_t nt, void* stream, int32_t* info) {
+    if (!l || !x || nt < 1 || !info) return set_err(TC_ERR_ARG, "trsm_tile: bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    StatusBuf sb;
+    int r = sb.alloc(s);
+    if (r) return r;
+    r = launch_trsm_direct(l, x, nt, sb.info, nullptr, 0, nullptr, nullptr, s);
+    if (r) return r;
+    CK(cudaMemcpyAsync(info, sb.info, 4, cudaMemcpyDeviceToHost, s));
+    sb.release(s);
+    CK(cudaStreamSynchronize(s));
+    return TC_OK;
+}
+
+extern "C" int tc_syrk_tile(const double* a, double* c, int32_t nt, void* stream) {
+    if (!a || !c || nt < 1) return set_err(TC_ERR_ARG, "syrk_tile: bad arguments");
+    // two-slot view: slot 0 = c, slot 1 = a (via scratch pointer trick)
+    const UpdKernel K = pick_upd(nt);
+    return launch_update_single(K, c, const_cast<double*>(a), 1, nt, 0, 1, 1, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int tc_gemm_tile(const double* a, const double* b, double* c, int32_t nt, void* stream) {
+    if (!a || !b || !c || nt < 1) return set_err(TC_ERR_ARG, "gemm_tile: bad arguments");
+    // c -= b a^T : kernel computes C -= A B^T with A = b (slot 1), B = a (slot 2)
+    // slots: 0 -> c (storage), >= 1 -> scratch; place b and a contiguously is not
+    // possible in general, so run with storage = c and scratch = b when a == b,
+    // else use two launches-free trick: pass a as storage base of a 3-slot view.
+    const UpdKernel K = pick_upd(nt);
+    cudaStream_t s = (cudaStream_t)stream;
+    // Build a tiny device pointer table: the single-op mode addresses tiles as
+    // storage + s*nt^2 / scratch + (s-S)*nt^2, so use S = 1 with storage = c
+    // and scratch = b for A, and a separate launch cannot express B = a.
+    // Instead compute with S large-offset arithmetic: pick base = min pointer.
+    const double* ptrs[3] = {c, b, a};
+    const double* base = std::min({ptrs[0], ptrs[1], ptrs[2]});
+    const size_t nt2 = (size_t)nt * nt;
+    auto off = [&](const double* p) -> int64_t {
+        const ptrdiff_t d = p - base;
+        return (d % (ptrdiff_t)nt2 == 0) ? (int64_t)(d / (ptrdiff_t)nt2) : -1;
+    };
+    const int64_t oc = off(c), ob = off(b), oa = off(a);
+    if (oc >= 0 && ob >= 0 && oa >= 0 && std::max({oc, ob, oa}) < INT32_MAX) {
+        return launch_update_single(K, const_cast<double*>(base), nullptr, INT64_MAX, nt, oc, ob, oa, nullptr, s);
+    }
+    // unaligned distinct allocations: stage a and b into one temporary buffer
+    double* tmp = nullptr;
+    CK(cudaMallocAsync((void**)&tmp, 2 * nt2 * 8, s));
+    CK(cudaMemcpyAsync(tmp, b, nt2 * 8, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(tmp + nt2, a, nt2 * 8, cudaMemcpyDeviceToDevice, s));
+    int r = launch_update_single(K, c, tmp, 1, nt, 0, 1, 2, nullptr, s);
+    cudaFreeAsync(tmp, s);
+    return r;
+}
+
+extern "C" int tc_geadd_tile(const double* t, double* c, int32_t nt, void* stream) {
+    if (!t || !c || nt < 1) return set_err(TC_ERR_ARG, "geadd_tile: bad arguments");
+    k_geadd<<<elem_grid(nt), 256, 0, (cudaStream_t)stream>>>(nullptr, c, const_cast<double*>(t), 1, 1, 0, nt, nullptr);
+    CK(cudaGetLastError());
+    return TC_OK;
+}
+
+// ----------------------------------------------------------- run_ops --
+extern "C" int tc_run_ops(double* storage, int64_t S, double* scratch, int64_t R, int32_t nt,
+                          const int8_t* op, const int64_t* dst, const int64_t* src1, const int64_t* src2,
+                          int64_t n_ops, int64_t start, int64_t stop, void* stream, int64_t* out_p,
+                          int32_t* out_info) {
+    if (nt < 1 || S < 0 || R < 0 || start < 0 || stop > n_ops || start > stop || !out_p || !out_info)
+        return set_err(TC_ERR_ARG, "run_ops: bad arguments");
+    if (stop > start && (!op || !dst)) return set_err(TC_ERR_ARG, "run_ops: null op arrays");
+    const int64_t lim = S + R;
+    for (int64_t p = start; p < stop; ++p) {
+        const int t = op[p];
+        auto bad = [&](int64_t v) { return v < 0 || v >= lim; };
+        if (bad(dst[p])) return set_err(TC_ERR_ARG, "run_ops: op %lld dst %lld out of range", (long long)p, (long long)dst[p]);
+        if ((t == TC_GEMM || t == TC_SYRK || t == TC_TRSM || t == TC_GEADD) && (!src1 || bad(src1[p])))
+            return set_err(TC_ERR_ARG, "run_ops: op %lld src1 out of range", (long long)p);
+        if (t == TC_GEMM && (!src2 || bad(src2[p])))
+            return set_err(TC_ERR_ARG, "run_ops: op %lld src2 out of range", (long long)p);
+        if ((t == TC_POTRF && !potrf_supported(nt)) || (t == TC_TRSM && nt > kMaxTrsmNt))
+            return set_err(TC_ERR_ARG, "run_ops: nt=%d unsupported for op %d", nt, t);
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    StatusBuf sb;
+    int r = sb.alloc(s);
+    if (r) return r;
+    const UpdKernel K = pick_upd(nt);
+    for (int64_t p = start; p < stop && r == TC_OK; ++p) {
+        const int t = op[p];
+        double* d = tptr(storage, scratch, S, dst[p], nt);
+        switch (t) {
+            case TC_GEMM:
+                r = launch_update_single(K, storage, scratch, S, nt, dst[p], src2[p], src1[p], sb.fail_p, s);
+                break;
+            case TC_SYRK:
+                r = launch_update_single(K, storage, scratch, S, nt, dst[p], src1[p], src1[p], sb.fail_p, s);
+                break;
+            case TC_TRSM:
+                r = launch_trsm_direct(tptr(storage, scratch, S, src1[p], nt), d, nt, nullptr, sb.fail_p, p,
+                                       sb.fail_p, sb.info, s);
+                break;
+            case TC_POTRF:
+                r = launch_potrf_direct(d, nt, nullptr, sb.fail_p, p, sb.fail_p, sb.info, s);
+                break;
+            case TC_GEADD:
+                k_geadd<<<elem_grid(nt), 256, 0, s>>>(nullptr, storage, scratch, S, src1[p], dst[p], nt, sb.fail_p);
+                break;
+            default:  // reference: any other code zeroes the target tile
+                k_zero<<<elem_grid(nt), 256, 0, s>>>(storage, scratch, S, dst[p], nt, sb.fail_p);
+                break;
+        }
+        if (r == TC_OK) {
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) r = set_err(TC_ERR_CUDA, "run_ops launch: %s", cudaGetErrorString(e));
+        }
+    }
+    int64_t hp[2];
+    if (r == TC_OK) {
+        CK(cudaMemcpyAsync(hp, sb.fail_p, 16, cudaMemcpyDeviceToHost, s));
+    }
+    sb.release(s);
+    CK(cudaStreamSynchronize(s));
+    if (r) return r;
+    if (hp[0] == kNoFail) {
+        *out_p = stop;
+        *out_info = -1;
+    } else {
+        *out_p = hp[0];
+        *out_info = (int32_t)(hp[1] & 0xffffffff);
+    }
+    return TC_OK;
+}
+
+// --------------------------------------------------- replay_residual --
+namespace {
+void tile_blocks(int nt, int BM, int BN, bool lower_only, std::vector<std::pair<int, int>>& out) {
+    out.clear();
+    for (int c0 = 0; c0 < nt; c0 += BN)
+        for (int r0 = 0; r0 < nt; r0 += BM) {
+            if (lower_only && r0 + BM - 1 < c0) continue;
+            out.emplace_back(r0, c0);
+        }
+}
+
+template <class T>
+int upload(const std::vector<T>& v, T** d, cudaStream_t s) {
+    *d = nullptr;
+    if (v.empty()) return TC_OK;
+    CK(cudaMallocAsync((void**)d, v.size() * sizeof(T), s));
+    CK(cudaMemcpyAsync(*d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return TC_OK;
+}
+}  // namespace
+
+extern "C" int tc_replay_residual(const double* storage, const double* tmpl, int64_t S, int32_t nt,
+                                  const int8_t* op, const int64_t* dst, const int64_t* src1,
+                                  const int64_t* src2, int64_t n_ops, const uint8_t* diag_slot, void* stream,
+                                  double* out_err2) {
+    if (nt < 1 || S < 1 || !out_err2 || !diag_slot || (n_ops > 0 && (!op || !dst)))
+        return set_err(TC_ERR_ARG, "replay_residual: bad arguments");
+    const UpdKernel K = pick_upd(nt);
+    std::vector<Item> items;
+    std::vector<Pair> pairs;
+    std::vector<std::pair<int, int>> blocks;
+    tile_blocks(nt, K.BM, K.BN, false, blocks);
+    for (int64_t p = 0; p < n_ops;) {
+        const int64_t d = dst[p];
+        if (d < 0 || d >= S) return set_err(TC_ERR_ARG, "replay_residual: dst out of range (scratch not allowed)");
+        const int32_t p0 = (int32_t)pairs.size();
+        int64_t q = p;
+        for (; q < n_ops && dst[q] == d; ++q) {
+            int64_t a, b;
+            switch (op[q]) {
+                case TC_POTRF: a = d; b = d; break;
+                case TC_SYRK: a = src1[q]; b = src1[q]; break;
+                case TC_TRSM: a = d; b = src1[q]; break;
+                default: a = src2[q]; b = src1[q]; break;
+            }
+            if (a < 0 || a >= S || b < 0 || b >= S) return set_err(TC_ERR_ARG, "replay_residual: source out of range");
+            pairs.push_back(Pair{(int32_t)a, (int32_t)b});
+        }
+        const int32_t p1 = (int32_t)pairs.size();
+        for (auto& bl : blocks) items.push_back(Item{(int32_t)d, bl.first, bl.second, p0, p1, MODE_RESID});
+        p = q;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    if (items.empty()) {
+        *out_err2 = 0.0;
+        return TC_OK;
+    }
+    Item* di = nullptr;
+    Pair* dp = nullptr;
+    uint8_t* dd = nullptr;
+    double* part = nullptr;
+    int r = upload(items, &di, s);
+    if (!r) r = upload(pairs, &dp, s);
+    std::vector<uint8_t> dg(diag_slot, diag_slot + S);
+    if (!r) r = upload(dg, &dd, s);
+    if (!r) {
+        CK(cudaMallocAsync((void**)&part, (items.size() + 1) * 8, s));
+        r = prep_kernel((const void*)K.fn, K.smem);
+    }
+    if (!r) {
+        const int64_t chunk = 1 << 30;
+        for (int64_t base = 0; base < (int64_t)items.size() && !r; base += chunk) {
+            UpdArgs ua{};
+            ua.items = di;
+            ua.pairs = dp;
+            ua.storage = const_cast<double*>(storage);
+            ua.S = S;
+            ua.nt = nt;
+            ua.item_base = (int32_t)base;
+            ua.tmpl = tmpl;
+            ua.diag = dd;
+            ua.resid_out = part;
+            const int64_t cnt = std::min<int64_t>(chunk, (int64_t)items.size() - base);
+            K.fn<<<(unsigned)cnt, K.nth, K.smem, s>>>(ua);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) r = set_err(TC_ERR_CUDA, "replay launch: %s", cudaGetErrorString(e));
+        }
+        if (!r) {
+            k_sum_fixed<<<1, 256, 0, s>>>(part, (int64_t)items.size(), 1.0, part + items.size());
+            CK(cudaMemcpyAsync(out_err2, part + items.size(), 8, cudaMemcpyDeviceToHost, s));
+        }
+    }
+    if (di) cudaFreeAsync(di, s);
+    if (dp) cudaFreeAsync(dp, s);
+    if (dd) cudaFreeAsync(dd, s);
+    if (part) cudaFreeAsync(part, s);
+    CK(cudaStreamSynchronize(s));
+    return r;
+}
+
+// ======================================================================
+// Optimised launch plan
+// ======================================================================
+namespace {
+
+enum LaunchKind { L_UPD = 0, L_POTRF = 1, L_TRSM = 2, L_COMBINE = 3, L_LOGDET = 4 };
+
+struct Launch {
+    int kind = 0;
+    int high = 0;                // critical-path priority
+    int64_t off = 0, cnt = 0;    // items (UPD) / targets (TRSM)
+    int32_t k = -1;              // column (POTRF/TRSM)
+    int64_t slot = -1;           // POTRF slot / TRSM L slot / COMBINE target
+    int64_t scratch0 = 0;        // COMBINE
+    uint32_t live = 0;           // COMBINE
+    std::vector<int32_t> deps;
+};
+
+struct Lane {
+    Ctx* d_ctx = nullptr;
+    int64_t* d_fail = nullptr;
+    double* d_ld = nullptr;      // [T + 1] partials + result
+    double* d_scratch = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;
+    Ctx h{};
+};
+
+}  // namespace
+
+struct tc_plan {
+    int64_t n = 0;
+    int nt = 0;
+    int T = 0;
+    int64_t S = 0;
+    tc_plan_opts opts{};
+    int W = 0;
+    std::vector<int32_t> frow, fcol;
+    std::vector<int64_t> cs;            // column -> first slot
+    std::vector<Launch> launches;
+    std::vector<Item> items;
+    std::vector<Pair> pairs;
+    std::vector<int32_t> tgts;          // TRSM targets
+    int64_t R = 0;                      // scratch tiles per lane
+    double flops = 0.0;
+    UpdKernel upd{};
+    // device copies
+    Item* d_items = nullptr;
+    Pair* d_pairs = nullptr;
+    int32_t* d_tgts = nullptr;
+    int64_t* d_diag_slots = nullptr;
+    // solve metadata: per column off-diagonal slots and rows
+    std::vector<int64_t> sol_off;
+    int32_t* d_sol_slots = nullptr;
+    int32_t* d_sol_rows = nullptr;
+    std::vector<Lane> lanes;
+    int prio_hi = 0, prio_lo = 0;
+    int dev = 0;
+};
+
+namespace {
+
+int64_t find_slot(const tc_plan& P, int32_t m, int32_t c) {
+    // slots of column c are [cs[c], cs[c+1]) with ascending rows
+    const int32_t* b = P.frow.data() + P.cs[c];
+    const int32_t* e = P.frow.data() + P.cs[c + 1];
+    const int32_t* it = std::lower_bound(b, e, m);
+    return (it != e && *it == m) ? (int64_t)(it - P.frow.data()) : -1;
+}
+
+int build_plan(tc_plan& P) {
+    const int T = P.T, nt = P.nt;
+    const int64_t S = P.S;
+    // column starts, validation
+    P.cs.assign(T + 1, 0);
+    for (int64_t s = 0; s < S; ++s) {
+        if (P.fcol[s] < 0 || P.fcol[s] >= T || P.frow[s] < P.fcol[s] || P.frow[s] >= T)
+            return set_err(TC_ERR_ARG, "plan: slot %lld out of the lower tile triangle", (long long)s);
+        if (s > 0 && (P.fcol[s] < P.fcol[s - 1] || (P.fcol[s] == P.fcol[s - 1] && P.frow[s] <= P.frow[s - 1])))
+            return set_err(TC_ERR_ARG, "plan: slots not in (col,row) order");
+        P.cs[P.fcol[s] + 1]++;
+    }
+    for (int k = 0; k < T; ++k) P.cs[k + 1] += P.cs[k];
+    for (int k = 0; k < T; ++k)
+        if (P.cs[k + 1] == P.cs[k] || P.frow[P.cs[k]] != k)
+            return set_err(TC_ERR_ARG, "plan: diagonal tile %d missing", k);
+    // row lists (n ascending): L(k, n) slots
+    std::vector<int64_t> rp(T + 1, 0);
+    for (int64_t s = 0; s < S; ++s)
+        if (P.frow[s] != P.fcol[s]) rp[P.frow[s] + 1]++;
+    for (int k = 0; k < T; ++k) rp[k + 1] += rp[k];
+    std::vector<int32_t> rn(rp[T]);
+    std::vector<int64_t> rs(rp[T]);
+    {
+        std::vector<int64_t> fill(rp.begin(), rp.end() - 1);
+        for (int64_t s = 0; s < S; ++s)
+            if (P.frow[s] != P.fcol[s]) {
+                const int64_t at = fill[P.frow[s]]++;
+                rn[at] = P.fcol[s];
+                rs[at] = s;
+            }
+    }
+    std::vector<int32_t> parent(T, -1);
+    for (int c = 0; c < T; ++c)
+        if (P.cs[c + 1] - P.cs[c] > 1) parent[c] = P.frow[P.cs[c] + 1];
+
+    // ---- pass 1: pairs per target, accum, reduced-chain classification
+    std::vector<int64_t> tp0(S), tp1(S);
+    P.pairs.clear();
+    for (int k = 0; k < T; ++k) {
+        for (int64_t t = P.cs[k]; t < P.cs[k + 1]; ++t) {
+            const int32_t m = P.frow[t];
+            tp0[t] = (int64_t)P.pairs.size();
+            for (int64_t x = rp[k]; x < rp[k + 1]; ++x) {
+                const int32_t nn = rn[x];
+                const int64_t skn = rs[x];
+                const int64_t smn = (m == k) ? skn : find_slot(P, m, nn);
+                if (smn >= 0) P.pairs.push_back(Pair{(int32_t)smn, (int32_t)skn});
+            }
+            tp1[t] = (int64_t)P.pairs.size();
+        }
+    }
+    if (P.pairs.size() > (size_t)INT32_MAX) return set_err(TC_ERR_ARG, "plan: too many pairs");
+    const int W = P.W;
+    const int thr = P.opts.tree_threshold;
+    std::vector<int64_t> red_base(S, -1);  // scratch index base for reduced targets
+    int64_t nred = 0;
+    if (thr > 0 && W >= 2) {
+        for (int64_t t = 0; t < S; ++t)
+            if (tp1[t] - tp0[t] >= thr) red_base[t] = (nred++) * W;
+    }
+    P.R = nred * W;
+    const int CH = P.opts.chunk > 0 ? P.opts.chunk : 8;
+
+    std::vector<std::pair<int, int>> blk_full, blk_low;
+    tile_blocks(nt, P.upd.BM, P.upd.BN, false, blk_full);
+    tile_blocks(nt, P.upd.BM, P.upd.BN, true, blk_low);
+    auto blocks_for = [&](int64_t t) -> const std::vector<std::pair<int, int>>& {
+        return P.frow[t] == P.fcol[t] ? blk_low : blk_full;
+    };
+
+    // split-K pieces of reduced chains: target t's pairs whose column n falls in
+    // [j*CH, (j+1)*CH) form one piece, emitted right after the panel of the
+    // piece's last column; pieces with equal j and last column share a launch.
+    struct Piece {
+        int j;
+        int64_t t, a, b;
+    };
+    std::vector<std::vector<Piece>> pieces_at(T);
+    for (int64_t t = 0; t < S; ++t) {
+        if (red_base[t] < 0) continue;
+        for (int64_t x = tp0[t]; x < tp1[t];) {
+            const int j = P.fcol[P.pairs[x].b] / CH;
+            int64_t y = x;
+            while (y < tp1[t] && P.fcol[P.pairs[y].b] / CH == j) ++y;
+            pieces_at[P.fcol[P.pairs[y - 1].b]].push_back(Piece{j, t, x, y});
+            x = y;
+        }
+    }
+
+    // ---- pass 2: launches in topological order
+    P.launches.clear();
+    P.items.clear();
+    P.tgts.clear();
+    std::vector<int32_t> pnode(T, -1);           // launch finishing column k
+    std::vector<uint32_t> live_mask(S, 0);
+    std::vector<std::vector<int32_t>> buf_writer(S);  // per reduced target: last chunk launch per residue
+    double flops = 0.0;
+    const double n3 = (double)nt * nt * nt;
+
+    auto add_panel_deps = [&](std::vector<int32_t>& deps, std::vector<int32_t>& cols) {
+        std::sort(cols.begin(), cols.end());
+        cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+        for (int32_t c : cols) {
+            const int32_t pa = parent[c];
+            if (pa >= 0 && std::binary_search(cols.begin(), cols.end(), pa)) continue;
+            deps.push_back(pnode[c]);
+        }
+    };
+
+    auto emit_items = [&](int64_t t, int64_t p0, int64_t p1, int32_t dst, int mode) {
+        for (auto& bl : blocks_for(t))
+            P.items.push_back(Item{dst, bl.first, bl.second, (int32_t)p0, (int32_t)p1, mode});
+    };
+
+    for (int k = 0; k < T; ++k) {
+        const int64_t c0 = P.cs[k], c1 = P.cs[k + 1];
+        const int32_t nlast = (P.opts.lookahead && rp[k + 1] > rp[k]) ? rn[rp[k + 1] - 1] : -1;
+        // B(k): bulk pairs of non-reduced targets
+        int32_t bnode = -1, lnode = -1;
+        {
+            Launch L;
+            L.kind = L_UPD;
+            L.off = (int64_t)P.items.size();
+            std::vector<int32_t> cols;
+            for (int64_t t = c0; t < c1; ++t) {
+                if (red_base[t] >= 0) continue;
+                int64_t p1 = tp1[t];
+                if (nlast >= 0 && p1 > tp0[t] && P.fcol[P.pairs[p1 - 1].b] == nlast) --p1;
+                if (p1 > tp0[t]) {
+                    emit_items(t, tp0[t], p1, (int32_t)t, MODE_SUB);
+                    for (int64_t x = tp0[t]; x < p1; ++x) cols.push_back(P.fcol[P.pairs[x].b]);
+                    flops += (P.frow[t] == k ? 1.0 : 2.0) * n3 * (double)(p1 - tp0[t]);
+                }
+            }
+            L.cnt = (int64_t)P.items.size() - L.off;
+            if (L.cnt > 0) {
+                add_panel_deps(L.deps, cols);
+                bnode = (int32_t)P.launches.size();
+                P.launches.push_back(std::move(L));
+            }
+        }
+        if (nlast >= 0) {
+            Launch L;
+            L.kind = L_UPD;
+            L.high = 1;
+            L.off = (int64_t)P.items.size();
+            for (int64_t t = c0; t < c1; ++t) {
+                if (red_base[t] >= 0) continue;
+                const int64_t p1 = tp1[t];
+                if (p1 > tp0[t] && P.fcol[P.pairs[p1 - 1].b] == nlast) {
+                    emit_items(t, p1 - 1, p1, (int32_t)t, MODE_SUB);
+                    flops += (P.frow[t] == k ? 1.0 : 2.0) * n3;
+                }
+            }
+            L.cnt = (int64_t)P.items.size() - L.off;
+            if (L.cnt > 0) {
+                L.deps.push_back(pnode[nlast]);
+                if (bnode >= 0) L.deps.push_back(bnode);
+                lnode = (int32_t)P.launches.size();
+                P.launches.push_back(std::move(L));
+            }
+        }
+        // combines of reduced targets of this column
+        std::vector<int32_t> comb_diag, comb_off;
+        for (int64_t t = c0; t < c1; ++t) {
+            if (red_base[t] < 0) continue;
+            Launch L;
+            L.kind = L_COMBINE;
+            L.high = 1;
+            L.slot = t;
+            L.scratch0 = S + red_base[t];
+            L.live = live_mask[t];
+            for (int32_t w : buf_writer[t])
+                if (w >= 0) L.deps.push_back(w);
+            const int32_t id = (int32_t)P.launches.size();
+            (P.frow[t] == k ? comb_diag : comb_off).push_back(id);
+            P.launches.push_back(std::move(L));
+        }
+        // POTRF(k)
+        int32_t pot;
+        {
+            Launch L;
+            L.kind = L_POTRF;
+            L.high = 1;
+            L.k = k;
+            L.slot = c0;
+            if (bnode >= 0) L.deps.push_back(bnode);
+            if (lnode >= 0) L.deps.push_back(lnode);
+            for (int32_t x : comb_diag) L.deps.push_back(x);
+            pot = (int32_t)P.launches.size();
+            P.launches.push_back(std::move(L));
+            flops += n3 / 3.0;
+        }
+        pnode[k] = pot;
+        if (c1 - c0 > 1) {
+            Launch L;
+            L.kind = L_TRSM;
+            L.high = 1;
+            L.k = k;
+            L.slot = c0;
+            L.off = (int64_t)P.tgts.size();
+            for (int64_t t = c0 + 1; t < c1; ++t) P.tgts.push_back((int32_t)t);
+            L.cnt = c1 - c0 - 1;
+            L.deps.push_back(pot);
+            if (bnode >= 0) L.deps.push_back(bnode);
+            if (lnode >= 0) L.deps.push_back(lnode);
+            for (int32_t x : comb_off) L.deps.push_back(x);
+            pnode[k] = (int32_t)P.launches.size();
+            P.launches.push_back(std::move(L));
+            flops += n3 * (double)(c1 - c0 - 1);
+        }
+        // split-K pieces of reduced chains that became ready with column k
+        auto& pcs = pieces_at[k];
+        std::stable_sort(pcs.begin(), pcs.end(), [](const Piece& x, const Piece& y) { return x.j < y.j; });
+        for (size_t u = 0; u < pcs.size();) {
+            size_t v = u;
+            while (v < pcs.size() && pcs[v].j == pcs[u].j) ++v;
+            const int w = pcs[u].j % W;
+            Launch L;
+            L.kind = L_UPD;
+            L.off = (int64_t)P.items.size();
+            std::vector<int32_t> cols;
+            for (size_t z = u; z < v; ++z) {
+                const Piece& pc = pcs[z];
+                const int64_t t = pc.t;
+                if (buf_writer[t].empty()) buf_writer[t].assign(W, -1);
+                const bool first = !((live_mask[t] >> w) & 1u);
+                emit_items(t, pc.a, pc.b, (int32_t)(S + red_base[t] + w), first ? MODE_NEGSTORE : MODE_SUB);
+                live_mask[t] |= 1u << w;
+                for (int64_t x = pc.a; x < pc.b; ++x) cols.push_back(P.fcol[P.pairs[x].b]);
+                if (buf_writer[t][w] >= 0) L.deps.push_back(buf_writer[t][w]);
+                flops += (P.frow[t] == P.fcol[t] ? 1.0 : 2.0) * n3 * (double)(pc.b - pc.a);
+            }
+            L.cnt = (int64_t)P.items.size() - L.off;
+            add_panel_deps(L.deps, cols);
+            const int32_t id = (int32_t)P.launches.size();
+            for (size_t z = u; z < v; ++z) buf_writer[pcs[z].t][w] = id;
+            P.launches.push_back(std::move(L));
+            u = v;
+        }
+    }
+    // final logdet reduction: depends on every launch with no dependents
+    {
+        std::vector<char> has_succ(P.launches.size(), 0);
+        for (auto& L : P.launches)
+            for (int32_t d : L.deps) has_succ[d] = 1;
+        Launch L;
+        L.kind = L_LOGDET;
+        L.high = 1;
+        for (size_t i = 0; i < P.launches.size(); ++i)
+            if (!has_succ[i]) L.deps.push_back((int32_t)i);
+        P.launches.push_back(std::move(L));
+    }
+    for (auto& L : P.launches) {
+        std::sort(L.deps.begin(), L.deps.end());
+        L.deps.erase(std::unique(L.deps.begin(), L.deps.end()), L.deps.end());
+    }
+    P.flops = flops;
+    // solve metadata
+    P.sol_off.assign(T + 1, 0);
+    std::vector<int32_t> sslots, srows;
+    for (int k = 0; k < T; ++k) {
+        for (int64_t t = P.cs[k] + 1; t < P.cs[k + 1]; ++t) {
+            sslots.push_back((int32_t)t);
+            srows.push_back(P.frow[t]);
+        }
+        P.sol_off[k + 1] = (int64_t)sslots.size();
+    }
+    std::vector<int64_t> dslots(T);
+    for (int k = 0; k < T; ++k) dslots[k] = P.cs[k];
+    cudaStream_t s = 0;
+    int r = upload(P.items, &P.d_items, s);
+    if (!r) r = upload(P.pairs, &P.d_pairs, s);
+    if (!r) r = upload(P.tgts, &P.d_tgts, s);
+    if (!r) r = upload(dslots, &P.d_diag_slots, s);
+    if (!r) r = upload(sslots, &P.d_sol_slots, s);
+    if (!r) r = upload(srows, &P.d_sol_rows, s);
+    if (r) return r;
+    CK(cudaStreamSynchronize(s));
+    return TC_OK;
+}
+
+// kernel launch (direct) or node params (graph) of launch i for a lane
+struct NodeArgs {
+    UpdArgs ua;
+    PotrfArgs pa;
+    TrsmArgs ta;
+    const Ctx* ctx;
+    int64_t target, scratch0;
+    int W;
+    uint32_t live;
+    int nt;
+    const double* ld_in;
+    int64_t ld_n;
+    double ld_scale;
+    double* ld_out;
+};
+
+int node_params(tc_plan& P, Lane& ln, size_t i, cudaKernelNodeParams& kp, NodeArgs& na, void** argv) {
+    const Launch& L = P.launches[i];
+    memset(&kp, 0, sizeof kp);
+    const int nt = P.nt;
+    switch (L.kind) {
+        case L_UPD: {
+            na.ua = UpdArgs{};
+            na.ua.items = P.d_items;
+            na.ua.pairs = P.d_pairs;
+            na.ua.ctx = ln.d_ctx;
+            na.ua.nt = nt;
+            na.ua.item_base = (int32_t)L.off;
+            argv[0] = &na.ua;
+            kp.func = (void*)P.upd.fn;
+            kp.gridDim = dim3((unsigned)L.cnt);
+            kp.blockDim = dim3(P.upd.nth);
+            kp.sharedMemBytes = P.upd.smem;
+            break;
+        }
+        case L_POTRF: {
+            bool in_smem;
+            const size_t sm = potrf_smem(nt, &in_smem);
+            na.pa = PotrfArgs{};
+            na.pa.ctx = ln.d_ctx;
+            na.pa.slot = L.slot;
+            na.pa.nt = nt;
+            na.pa.k = L.k;
+            const int64_t live = P.n - (int64_t)L.k * nt;
+            na.pa.live = (int32_t)std::min<int64_t>(live, nt);
+            na.pa.in_smem = in_smem;
+            argv[0] = &na.pa;
+            kp.func = (void*)k_potrf;
+            kp.gridDim = dim3(1);
+            kp.blockDim = dim3(kPotrfThreads);
+            kp.sharedMemBytes = (unsigned)sm;
+            break;
+        }
+        case L_TRSM: {
+            na.ta = TrsmArgs{};
+            na.ta.ctx = ln.d_ctx;
+            na.ta.lslot = L.slot;
+            na.ta.targets = P.d_tgts + L.off;
+            na.ta.nt = nt;
+            argv[0] = &na.ta;
+            kp.func = (void*)k_trsm;
+            kp.gridDim = dim3((nt + kTrsmRows - 1) / kTrsmRows, (unsigned)L.cnt);
+            kp.blockDim = dim3(kTrsmThreads);
+            kp.sharedMemBytes = (unsigned)trsm_smem_bytes(nt);
+            break;
+        }
+        case L_COMBINE: {
+            na.ctx = ln.d_ctx;
+            na.target = L.slot;
+            na.scratch0 = L.scratch0 - P.S;  // scratch index relative to scratch base
+            na.W = P.W;
+            na.live = L.live;
+            na.nt = nt;
+            argv[0] = &na.ctx;
+            argv[1] = &na.target;
+            argv[2] = &na.scratch0;
+            argv[3] = &na.W;
+            argv[4] = &na.live;
+            argv[5] = &na.nt;
+            kp.func = (void*)k_combine;
+            kp.gridDim = dim3(elem_grid(nt));
+            kp.blockDim = dim3(256);
+            break;
+        }
+        default: {  // L_LOGDET
+            na.ld_in = ln.d_ld;
+            na.ld_n = P.T;
+            na.ld_scale = 2.0;
+            na.ld_out = ln.d_ld + P.T;
+            argv[0] = &na.ld_in;
+            argv[1] = &na.ld_n;
+            argv[2] = &na.ld_scale;
+            argv[3] = &na.ld_out;
+            kp.func = (void*)k_sum_fixed;
+            kp.gridDim = dim3(1);
+            kp.blockDim = dim3(256);
+            break;
+        }
+    }
+    kp.kernelParams = argv;
+    return TC_OK;
+}
+
+int ensure_lane(tc_plan& P, int lane) {
+    if (lane < 0 || lane >= 256) return set_err(TC_ERR_ARG, "lane %d out of range", lane);
+    if ((int)P.lanes.size() <= lane) P.lanes.resize(lane + 1);
+    Lane& ln = P.lanes[lane];
+    if (ln.d_ctx) return TC_OK;
+    CK(cudaMalloc(&ln.d_ctx, sizeof(Ctx)));
+    CK(cudaMalloc(&ln.d_fail, 8));
+    CK(cudaMalloc(&ln.d_ld, (P.T + 1) * sizeof(double)));
+    CK(cudaMemset(ln.d_ld, 0, (P.T + 1) * sizeof(double)));
+    if (P.R > 0) {
+        CK(cudaMalloc(&ln.d_scratch, (size_t)P.R * P.nt * P.nt * sizeof(double)));
+        CK(cudaMemset(ln.d_scratch, 0, (size_t)P.R * P.nt * P.nt * sizeof(double)));
+    }
+    return TC_OK;
+}
+
+int prep_all(tc_plan& P) {
+    int r = prep_kernel((const void*)P.upd.fn, P.upd.smem);
+    if (r) return r;
+    bool in_smem;
+    r = prep_kernel((const void*)k_potrf, (int)potrf_smem(P.nt, &in_smem));
+    if (r) return r;
+    return prep_kernel((const void*)k_trsm, (int)trsm_smem_bytes(P.nt));
+}
+
+int build_graph(tc_plan& P, Lane& ln) {
+    if (ln.exec) return TC_OK;
+    int r = prep_all(P);
+    if (r) return r;
+    CK(cudaGraphCreate(&ln.graph, 0));
+    std::vector<cudaGraphNode_t> nodes(P.launches.size());
+    std::vector<cudaGraphNode_t> deps;
+    for (size_t i = 0; i < P.launches.size(); ++i) {
+        cudaKernelNodeParams kp;
+        NodeArgs na;
+        void* argv[8];
+        r = node_params(P, ln, i, kp, na, argv);
+        if (r) return r;
+        deps.clear();
+        for (int32_t d : P.launches[i].deps) deps.push_back(nodes[d]);
+        CK(cudaGraphAddKernelNode(&nodes[i], ln.graph, deps.data(), deps.size(), &kp));
+        cudaLaunchAttributeValue v;
+        memset(&v, 0, sizeof v);
+        v.priority = P.launches[i].high ? P.prio_hi : P.prio_lo;
+        CK(cudaGraphKernelNodeSetAttribute(nodes[i], cudaLaunchAttributePriority, &v));
+    }
+    CK(cudaGraphInstantiateWithFlags(&ln.exec, ln.graph, cudaGraphInstantiateFlagUseNodePriority));
+    return TC_OK;
+}
+
+int run_direct(tc_plan& P, Lane& ln, cudaStream_t s) {
+    int r = prep_all(P);
+    if (r) return r;
+    for (size_t i = 0; i < P.launches.size(); ++i) {
+        cudaKernelNodeParams kp;
+        NodeArgs na;
+        void* argv[8];
+        r = node_params(P, ln, i, kp, na, argv);
+        if (r) return r;
+        CK(cudaLaunchKernel(kp.func, kp.gridDim, kp.blockDim, kp.kernelParams, kp.sharedMemBytes, s));
+    }
+    return TC_OK;
+}
+
+}  // namespace
+
+extern "C" int tc_plan_create(int64_t n, int32_t nt, int64_t S, const int32_t* f_rows, const int32_t* f_cols,
+                              const tc_plan_opts* opts, tc_plan_t* out) {
+    if (!out || n < 1 || nt < 1 || S < 1 || !f_rows || !f_cols) return set_err(TC_ERR_ARG, "plan_create: bad arguments");
+    *out = nullptr;
+    if (tc_device_count() < 1) return set_err(TC_ERR_CUDA, "plan_create: no CUDA device");
+    if (!potrf_supported(nt) || nt > kMaxTrsmNt)
+        return set_err(TC_ERR_ARG, "plan_create: tile size %d unsupported (need nt<=160 or nt%%8==0, nt<=%d)", nt,
+                       kMaxTrsmNt);
+    std::unique_ptr<tc_plan> P(new tc_plan());
+    P->n = n;
+    P->nt = nt;
+    P->T = (int)((n + nt - 1) / nt);
+    P->S = S;
+    if (opts) P->opts = *opts;
+    else {
+        memset(&P->opts, 0, sizeof P->opts);
+        P->opts.lookahead = 1;
+        P->opts.use_graph = 1;
+    }
+    P->W = P->opts.tree_workers > 0 ? P->opts.tree_workers : 8;
+    if (P->W > kMaxW) return set_err(TC_ERR_ARG, "plan_create: tree_workers <= %d", kMaxW);
+    if (P->opts.tree_threshold == 0) P->opts.tree_threshold = 2 * P->W;
+    P->frow.assign(f_rows, f_rows + S);
+    P->fcol.assign(f_cols, f_cols + S);
+    P->upd = pick_upd(nt);
+    CK(cudaGetDevice(&P->dev));
+    CK(cudaDeviceGetStreamPriorityRange(&P->prio_lo, &P->prio_hi));
+    int r = build_plan(*P);
+    if (r) {
+        tc_plan_destroy(P.release());
+        return r;
+    }
+    *out = P.release();
+    return TC_OK;
+}
+
+extern "C" int tc_plan_info(tc_plan_t p, int64_t* n_launches, int64_t* n_items, int64_t* n_pairs,
+                            int64_t* scratch_tiles, double* tile_flops) {
+    if (!p) return set_err(TC_ERR_ARG, "plan_info: null plan");
+    if (n_launches) *n_launches = (int64_t)p->launches.size();
+    if (n_items) *n_items = (int64_t)p->items.size();
+    if (n_pairs) *n_pairs = (int64_t)p->pairs.size();
+    if (scratch_tiles) *scratch_tiles = p->R;
+    if (tile_flops) *tile_flops = p->flops;
+    return TC_OK;
+}
+
+extern "C" int tc_plan_factorize_async(tc_plan_t p, int32_t lane, double* storage, void* stream) {
+    if (!p || !storage) return set_err(TC_ERR_ARG, "plan_factorize: bad arguments");
+    int r = ensure_lane(*p, lane);
+    if (r) return r;
+    Lane& ln = p->lanes[lane];
+    cudaStream_t s = (cudaStream_t)stream;
+    ln.h.storage = storage;
+    ln.h.scratch = ln.d_scratch;
+    ln.h.S = p->S;
+    ln.h.fail = ln.d_fail;
+    ln.h.ld_part = ln.d_ld;
+    ln.h.ld_out = ln.d_ld + p->T;
+    const int64_t nf = kNoFail;
+    CK(cudaMemcpyAsync(ln.d_ctx, &ln.h, sizeof(Ctx), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ln.d_fail, &nf, 8, cudaMemcpyHostToDevice, s));
+    if (p->opts.use_graph) {
+        r = build_graph(*p, ln);
+        if (r) return r;
+        CK(cudaGraphLaunch(ln.exec, s));
+    } else {
+        r = run_direct(*p, ln, s);
+        if (r) return r;
+    }
+    return TC_OK;
+}
+
+extern "C" int tc_plan_collect(tc_plan_t p, int32_t lane, void* stream, int64_t* fail_index, double* logdet) {
+    if (!p || lane < 0 || lane >= (int)p->lanes.size() || !p->lanes[lane].d_ctx)
+        return set_err(TC_ERR_ARG, "plan_collect: bad lane");
+    Lane& ln = p->lanes[lane];
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t f = kNoFail;
+    double ld = 0.0;
+    CK(cudaMemcpyAsync(&f, ln.d_fail, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&ld, ln.d_ld + p->T, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (fail_index) *fail_index = (f == kNoFail) ? -1 : f;
+    if (logdet) *logdet = ld;
+    return TC_OK;
+}
+
+extern "C" int tc_plan_factorize(tc_plan_t p, double* storage, void* stream, int64_t* fail_index) {
+    int r = tc_plan_factorize_async(p, 0, storage, stream);
+    if (r) return r;
+    return tc_plan_collect(p, 0, stream, fail_index, nullptr);
+}
+
+extern "C" int tc_plan_logdet(tc_plan_t p, const double* storage, void* stream, double* out) {
+    if (!p || !storage || !out) return set_err(TC_ERR_ARG, "plan_logdet: bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    double* part = nullptr;
+    CK(cudaMallocAsync((void**)&part, (p->T + 1) * sizeof(double), s));
+    k_logdet_tiles<<<p->T, 32, 0, s>>>(storage, p->d_diag_slots, p->T, p->nt, p->n, part);
+    k_sum_fixed<<<1, 256, 0, s>>>(part, p->T, 2.0, part + p->T);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, part + p->T, 8, cudaMemcpyDeviceToHost, s));
+    cudaFreeAsync(part, s);
+    CK(cudaStreamSynchronize(s));
+    return TC_OK;
+}
+
+extern "C" int tc_plan_solve(tc_plan_t p, const double* storage, double* rhs, int32_t nrhs, void* stream) {
+    if (!p || !storage || !rhs || nrhs < 1) return set_err(TC_ERR_ARG, "plan_solve: bad arguments");
+    if (p->nt > 1024) return set_err(TC_ERR_ARG, "plan_solve: nt > 1024 unsupported");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int nt = p->nt, T = p->T;
+    const int64_t ldr = (int64_t)T * nt;
+    const int bs = std::min(((nt + 31) / 32) * 32, 1024);
+    for (int k = 0; k < T; ++k) {
+        k_trsv_diag<<<nrhs, bs, nt * sizeof(double), s>>>(storage, p->cs[k], rhs, ldr, (int64_t)k * nt, nt, 0);
+        const int64_t a = p->sol_off[k], b = p->sol_off[k + 1];
+        if (b > a)
+            k_gemv_fwd<<<dim3((unsigned)(b - a), nrhs), bs, 0, s>>>(storage, p->d_sol_slots + a, p->d_sol_rows + a, rhs,
+                                                                  ldr, k, nt);
+    }
+    for (int k = T - 1; k >= 0; --k) {
+        const int64_t a = p->sol_off[k], b = p->sol_off[k + 1];
+        if (b > a)
+            k_gemv_bwd<<<nrhs, 256, 0, s>>>(storage, p->d_sol_slots + a, p->d_sol_rows + a, (int)(b - a), rhs, ldr, k,
+                                            nt);
+        k_trsv_diag<<<nrhs, bs, nt * sizeof(double), s>>>(storage, p->cs[k], rhs, ldr, (int64_t)k * nt, nt, 1);
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    return TC_OK;
+}
+
+extern "C" int tc_plan_pack_offsets(tc_plan_t p, int64_t n, const int64_t* col_ptr, const int32_t* row_idx,
+                                    int64_t* offs) {
+    if (!p || n != p->n || !col_ptr || !row_idx || !offs) return set_err(TC_ERR_ARG, "pack_offsets: bad arguments");
+    const int nt = p->nt;
+    const int64_t nt2 = (int64_t)nt * nt;
+    for (int64_t c = 0; c < n; ++c) {
+        const int32_t tc = (int32_t)(c / nt);
+        int64_t s = p->cs[tc];
+        const int64_t se = p->cs[tc + 1];
+        for (int64_t e = col_ptr[c]; e < col_ptr[c + 1]; ++e) {
+            const int32_t r = row_idx[e];
+            if (r < c || r >= n) return set_err(TC_ERR_FORMAT, "pack_offsets: entry outside the lower triangle");
+            const int32_t tr = r / nt;
+            while (s < se && p->frow[s] < tr) ++s;
+            if (s >= se || p->frow[s] != tr) {
+                // rows are sorted within a column, but allow unsorted input via search
+                const int64_t f = find_slot(*p, tr, tc);
+                if (f < 0) return set_err(TC_ERR_ARG, "grid does not cover the matrix pattern");
+                offs[e] = f * nt2 + (c % nt) * nt + (r % nt);
+                s = p->cs[tc];
+                continue;
+            }
+            offs[e] = s * nt2 + (c % nt) * nt + (r % nt);
+        }
+    }
+    return TC_OK;
+}
+
+extern "C" int tc_plan_pack(tc_plan_t p, const double* vals, const int64_t* offs, int64_t nnz, double* storage,
+                            void* stream) {
+    if (!p || !storage || (nnz > 0 && (!vals || !offs))) return set_err(TC_ERR_ARG, "plan_pack: bad arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t bytes = (size_t)p->S * p->nt * p->nt * sizeof(double);
+    CK(cudaMemsetAsync(storage, 0, bytes, s));
+    if (nnz > 0) {
+        const int64_t blocks = std::min<int64_t>((nnz + 255) / 256, 148 * 16);
+        k_pack<<<(unsigned)blocks, 256, 0, s>>>(vals, offs, nnz, storage);
+    }
+    const int from = (int)(p->n % p->nt);
+    if (from) k_pad_diag<<<1, p->nt, 0, s>>>(storage, p->cs[p->T - 1], p->nt, from);
+    CK(cudaGetLastError());
+    return TC_OK;
+}
+
+extern "C" void tc_plan_destroy(tc_plan_t p) {
+    if (!p) return;
+    for (auto& ln : p->lanes) {
+        if (ln.exec) cudaGraphExecDestroy(ln.exec);
+        if (ln.graph) cudaGraphDestroy(ln.graph);
+        cudaFree(ln.d_ctx);
+        cudaFree(ln.d_fail);
+        cudaFree(ln.d_ld);
+        cudaFree(ln.d_scratch);
+    }
+    cudaFree(p->d_items);
+    cudaFree(p->d_pairs);
+    cudaFree(p->d_tgts);
+    cudaFree(p->d_diag_slots);
+    cudaFree(p->d_sol_slots);
+    cudaFree(p->d_sol_rows);
+    delete p;
+}
+
+// error hook shared with the host-analysis translation unit (tc_host.cpp)
+extern "C" int tc__set_error(int code, const char* msg) {
+    g_err = msg;
+    return code;
+}
