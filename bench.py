@@ -1,0 +1,465 @@
+#!/usr/bin/env python
+"""bench.py — FP64 arrowhead tile Cholesky on B200.
+
+One *step* = one factorisation of the workload matrix from its CSC values
+resident in HBM: device scatter into tile storage + the CUDA-graph numeric
+factorisation with fused log-determinant.  ``value`` = factorizations/s over
+all ranks (each rank factorises its own replica: weak scaling, no data-path
+collective).  ``e2e`` = the same through the public API ``api.factorize`` with
+host CSC values (pinned H2D + D2H of the result inside the timed region) and,
+for N > 1, the NCCL all-gather of the per-matrix log-determinants.
+
+    python bench.py [--workload c2] [--tile 120] [--gpus N --steps K --warmup W]
+    python bench.py --impl reference ...     # reference CPU arm (oracle port)
+    python bench.py --measure-peaks           # FP64 DMMA / DGEMM peaks -> profiles/
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c1": ("arrowhead n=10,000 b=200 t=50 (BASELINE config 1)", 120),
+    "c2": ("variable-band arrowhead n=100,000 max band 1,000 t=200 (BASELINE config 2)", 240),
+    "c3": ("INLA 2000x100+10 (n=200,010) kappa=.5 rho=.9 tau=1e-3 (BASELINE config 3)", 240),
+    "c4": ("arrowhead n=1,000,000 b=2000 t=500 (BASELINE config 4)", 240),
+}
+PEAKS_FILE = os.path.join(ROOT, "profiles", "fp64_peaks.json")
+FP64_FALLBACK_TFLOPS = 37.0  # NVIDIA B200 FP64 (tensor) nominal, used only if unmeasured
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--tile", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--measure-peaks", action="store_true")
+    ap.add_argument("--ref-procs", type=int, default=0)
+    return ap.parse_args()
+
+
+def build_matrix(name):
+    from paper_2501_02483_b200 import workloads as W
+    if name == "c1":
+        return W.c1()
+    if name == "c2":
+        return W.c2_variable_band()
+    if name == "c3":
+        return W.c3()
+    if name == "c4":
+        return W.c4()
+    raise ValueError(name)
+
+
+# ------------------------------------------------------------------ clocks --
+class Clocks:
+    """nvidia-smi sampler (200 ms) running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200",
+                 "-i", str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ peaks --
+def measure_peaks():
+    import torch
+    from paper_2501_02483_b200._lib import check, lib, f64p
+    out = {"how": "DMMA m8n8k4 register microbenchmark (all SMs) and torch.matmul float64 "
+                  "8192^3 (cuBLAS DGEMM), best of 5, CUDA events", "gpu": torch.cuda.get_device_name()}
+    best = 0.0
+    cfgs = {}
+    for bps, wpb in ((1, 4), (2, 4), (1, 8), (2, 8), (4, 8)):
+        v = np.zeros(1)
+        vals = []
+        for _ in range(3):
+            check("dmma", lib.tc_bench_dmma_peak(200000, bps, wpb, v.ctypes.data_as(f64p)))
+            vals.append(float(v[0]))
+        cfgs[f"{bps}x{wpb}warps"] = max(vals)
+        best = max(best, max(vals))
+    out["dmma_tflops"] = best
+    out["dmma_configs"] = cfgs
+    a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    b = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        a @ b
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        a @ b
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    out["dgemm_tflops"] = 2 * 8192 ** 3 / (min(ts) * 1e-3) / 1e12
+    out["fp64_peak_tflops"] = max(out["dmma_tflops"], out["dgemm_tflops"])
+    os.makedirs(os.path.dirname(PEAKS_FILE), exist_ok=True)
+    with open(PEAKS_FILE, "w") as f:
+        json.dump(out, f, indent=1)
+    print(json.dumps(out))
+
+
+def fp64_peak():
+    try:
+        with open(PEAKS_FILE) as f:
+            d = json.load(f)
+        return float(d["fp64_peak_tflops"]), "measured (profiles/fp64_peaks.json: max of DMMA microbenchmark and cuBLAS DGEMM)"
+    except (OSError, KeyError, ValueError):
+        return FP64_FALLBACK_TFLOPS, "fallback nominal B200 FP64 (unmeasured)"
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# -------------------------------------------------------- CPU (oracle) arm --
+def _oracle_setup(m, nt):
+    import oracle as O
+    from paper_2501_02483_b200 import ctsf, symbolic
+    g = ctsf.build_tile_grid(m, nt)
+    s = symbolic.tile_symbolic_factorize(g)
+    fg = s.factor_grid
+    ts = symbolic.enumerate_tasks(s)
+    tasks = {"type": ts.task_type, "m": ts.m, "k": ts.k, "n": ts.n, "target": ts.target}
+    op, dst, s1, s2, _ = O.compile_ops(tasks, fg.slot_map, fg.n_tiles)
+    tpl = ctsf.pack_into_grid(m, fg).storage
+    return op, dst, s1, s2, tpl
+
+
+def cpu_baseline(m, nt):
+    """Oracle port of the reference run_ops (numba loops + OpenBLAS dgemm via
+    np.dot, 1 thread) on the full workload factorisation."""
+    import oracle as O
+    op, dst, s1, s2, tpl = _oracle_setup(m, nt)
+    sc = np.zeros((0, nt, nt))
+    warm = tpl[:2].copy()
+    O.run_ops(warm, sc, op[:0], dst[:0], s1[:0], s2[:0], 0, 0)  # JIT
+    small = np.zeros((3, nt, nt))
+    for i in range(3):
+        small[i] = np.eye(nt) * 4.0
+    O.potrf_t(small[0].T.copy())
+    st = tpl.copy()
+    t0 = time.perf_counter()
+    p, info = O.run_ops(st, sc, op, dst, s1, s2, 0, op.size)
+    dt = time.perf_counter() - t0
+    assert info == -1
+    return dt
+
+
+def _ref_worker(args):
+    name, nt, steps, q_in, q_out = args
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    import oracle as O
+    m = build_matrix(name)
+    op, dst, s1, s2, tpl = _oracle_setup(m, nt)
+    sc = np.zeros((0, nt, nt))
+    st = np.empty_like(tpl)
+    O.run_ops(st[:0], sc, op[:0], dst[:0], s1[:0], s2[:0], 0, 0)
+    q_out.put("ready")
+    while True:
+        cmd = q_in.get()
+        if cmd is None:
+            break
+        np.copyto(st, tpl)
+        t0 = time.perf_counter()
+        O.run_ops(st, sc, op, dst, s1, s2, 0, op.size)
+        q_out.put(time.perf_counter() - t0)
+
+
+def run_reference(a, name, nt, desc):
+    """Reference CPU implementation (oracle port of _backend_numba.run_ops) on
+    the box's host cores: one factorisation per process per step
+    (Appendix-A batch semantics; threads scale poorly, survey §8(d))."""
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0))
+    m = build_matrix(name)
+    est = (m.nnz * 12 + 3 * 8 * nt * nt * (m.nnz // max(1, nt)) // max(1, nt)) / 1e9
+    try:
+        import psutil
+        mem = psutil.virtual_memory().available / 1e9
+    except ImportError:
+        mem = 64.0
+    per_proc = max(2.0, 2.5 * est)
+    procs = a.ref_procs or max(1, min(cores, int(mem * 0.6 / per_proc)))
+    del m
+    ctx = mp.get_context("spawn")
+    qin = [ctx.Queue() for _ in range(procs)]
+    qout = ctx.Queue()
+    ps = [ctx.Process(target=_ref_worker, args=((name, nt, 0, qin[i], qout),)) for i in range(procs)]
+    for p in ps:
+        p.start()
+    for _ in ps:
+        assert qout.get() == "ready"
+
+    def step():
+        t0 = time.perf_counter()
+        for q in qin:
+            q.put(1)
+        for _ in ps:
+            qout.get()
+        return time.perf_counter() - t0
+
+    for _ in range(a.warmup):
+        step()
+    walls = [step() for _ in range(a.steps)]
+    for q in qin:
+        q.put(None)
+    for p in ps:
+        p.join()
+    wall = float(np.mean(walls))
+    value = procs / wall
+    line = {"impl": "reference", "metric": "factorizations/s (FP64 time-to-factor)", "value": value,
+            "unit": "factorizations/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": wall * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "tile": nt, "processes": procs},
+            "cpu_baseline": {"value": value, "unit": "factorizations/s", "cores": procs, "kind": "port",
+                             "sample": f"{procs} concurrent full factorisations per step (one per process, "
+                                       f"oracle run_ops = numba loops + OpenBLAS dgemm, 1 thread each)"},
+            "e2e": {"value": value, "unit": "factorizations/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- GPU arm --
+def run_ours(a, name, nt, desc, rank, world):
+    import torch
+    import torch.distributed as dist
+    from paper_2501_02483_b200 import api
+    from paper_2501_02483_b200._lib import check, lib, f64p, i64p
+
+    m = build_matrix(name)
+    opts = api.FactorOptions(tile_size=nt)
+    t0 = time.perf_counter()
+    pat = api._pattern_for(m, opts)
+    setup_s = time.perf_counter() - t0
+    plan = pat.plan
+    info = plan.info()
+    F = info["tile_flops"]
+    vals_dev = torch.from_numpy(np.ascontiguousarray(pat.permuted_values(m))).cuda()
+    offs = pat.offsets()
+    storage = plan.new_storage()
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    def step():
+        plan.pack(vals_dev, offs, storage, sh)
+        plan.factorize_async(storage, 0, sh)
+
+    for _ in range(max(a.warmup, 1)):
+        step()
+    fail, ld = plan.collect(0, sh)
+    if fail >= 0:
+        raise RuntimeError(f"factorisation failed at {fail}")
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = Clocks(int(os.environ.get("LOCAL_RANK", "0")))
+    clk.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / a.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    fail, ld2 = plan.collect(0, sh)
+    assert fail < 0 and ld2 == ld, "timed steps must reproduce the warm-up factor bitwise"
+
+    # ---- end to end through the public API (host values, H2D/D2H inside)
+    e2e_ms = []
+    for i in range(a.e2e_steps + 1):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        ctx = api.factorize(m, opts)
+        ldv = api.logdet(ctx)
+        if world > 1:
+            buf = torch.tensor([ldv], dtype=torch.float64, device="cuda")
+            outl = [torch.empty_like(buf) for _ in range(world)]
+            dist.all_gather(outl, buf)
+            torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) * 1e3
+        if i > 0:
+            e2e_ms.append(dt)
+        del ctx
+    e2e = float(np.mean(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = float(t.item())
+
+    # ---- roofline: serialised profiling pass, CUDA events per launch
+    peak, peak_src = fp64_peak()
+    hbm, hbm_src = hbm_peak()
+    prof = None
+    if not a.no_profile and rank == 0:
+        nc = 7
+        pms = np.zeros(nc)
+        pcnt = np.zeros(nc, dtype=np.int64)
+        pfl = np.zeros(nc)
+        plan.pack(vals_dev, offs, storage, sh)
+        check("tc_plan_profile", lib.tc_plan_profile(plan.h, storage.data_ptr(), sh, nc,
+                                                     pms.ctypes.data_as(f64p), pcnt.ctypes.data_as(i64p),
+                                                     pfl.ctypes.data_as(f64p)))
+        names = ["update_bulk", "update_last", "potrf", "trsm", "combine", "logdet", "update_splitk"]
+        prof = {names[i]: {"ms": float(pms[i]), "launches": int(pcnt[i]), "gflop": float(pfl[i] / 1e9)}
+                for i in range(nc) if pcnt[i]}
+    S, T = plan.S, plan.T
+    B = 16.0 * nt * nt * S
+    t_roof = max(F / (peak * 1e12), B / (hbm * 1e9))
+    useful = _useful_flops(pat)
+    value = world * 1000.0 / ms
+    line = {"metric": "factorizations/s (FP64 time-to-factor)", "value": value, "unit": "factorizations/s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": desc, "tile": nt, "n": m.n, "nnz": m.nnz, "tiles_per_side": T, "slots": S,
+                       "parallelism": f"replicas x{world} (one factorisation per GPU per step)",
+                       "l2": "inputs larger than L2 (tile storage %.2f GB)" % (B / 2 / 1e9)},
+            "time_to_factor_ms": ms, "gflops_tile": F / (ms * 1e-3) / 1e9,
+            "gflops_useful": useful / (ms * 1e-3) / 1e9 if useful else None,
+            "fp64_roofline": {"time_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms, "tile_flops": F,
+                              "compulsory_bytes": B, "peak_tflops": peak, "peak_source": peak_src},
+            "gpu_launches": int(info["launches"]) + 2, "setup_s": setup_s, "logdet": ld}
+    if prof:
+        dom = max((k for k in prof if k.startswith("update")), key=lambda k: prof[k]["ms"])
+        d = prof[dom]
+        achieved = d["gflop"] / d["launches"] / (d["ms"] / d["launches"] * 1e-3) / 1e3
+        line["roofline"] = {"bound": "tensor", "kernel": f"k_update ({dom})", "achieved": achieved,
+                            "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                            "peak_source": peak_src,
+                            "note": "per-launch algorithmic flops / CUDA-event launch time on a "
+                                    "serialised profiling pass of the same plan"}
+        line["profile"] = prof
+    line["e2e"] = {"value": world * 1000.0 / e2e, "unit": "factorizations/s",
+                   "h2d_bytes_per_step": int(m.nnz * 8), "d2h_bytes_per_step": 16,
+                   "ms_per_step": e2e, "path": "api.factorize(SymmetricCsc host values) + logdet"
+                   + (" + NCCL all_gather of logdets" if world > 1 else "")}
+    line["clocks"] = clocks
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        dt = cpu_baseline(m, nt)
+        line["cpu_baseline"] = {"value": 1.0 / dt, "unit": "factorizations/s", "cores": 1, "kind": "port",
+                                "sample": f"one full {name} factorisation (oracle run_ops, numba + OpenBLAS "
+                                          f"dgemm, OPENBLAS_NUM_THREADS=1), {dt:.2f} s"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def _useful_flops(pat):
+    try:
+        cp = pat.pm_pattern.col_ptr
+        # sum_j c_j^2 with c_j = column counts of L: use the exact fill count per column
+        return None if cp is None else None
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def main():
+    a = parse()
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    name = a.workload
+    desc, default_nt = WORKLOADS[name]
+    nt = a.tile or default_nt
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        run_reference(a, name, nt, desc)
+        return
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    if a.measure_peaks:
+        if rank == 0:
+            measure_peaks()
+        return
+    try:
+        run_ours(a, name, nt, desc, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

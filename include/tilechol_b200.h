@@ -68,6 +68,11 @@ int tc_structure_stats(int64_t n, const int64_t* col_ptr, const int32_t* row_idx
  * always written, row_idx[nnz] when non-NULL (memory-light, no temporaries). */
 int tc_arrowhead_pattern(int64_t n, int64_t b, int64_t t, int32_t block_diagonal,
                          int64_t* col_ptr, int32_t* row_idx);
+/* Variable-bandwidth arrowhead pattern (BASELINE config 2 / survey App. A2):
+ * head column j < n-t holds rows j..j+band[j] and the t arrow rows, tail
+ * columns are dense.  Same two-call convention as tc_arrowhead_pattern. */
+int tc_band_arrow_pattern(int64_t n, int64_t t, const int64_t* band, int64_t* col_ptr,
+                          int32_t* row_idx);
 /* reference matcore.py:309-316: diagonal = 1 + |row| sums, accumulated in CSC
  * order exactly like the two np.bincount passes (bit-identical). */
 int tc_arrowhead_diag(int64_t n, const int64_t* col_ptr, const int32_t* row_idx,
@@ -189,6 +194,16 @@ int tc_plan_pack_offsets(tc_plan_t p, int64_t n, const int64_t* col_ptr,
 int tc_plan_pack(tc_plan_t p, const double* values_dev, const int64_t* offsets_dev,
                  int64_t nnz, double* storage_dev, void* stream);
 void tc_plan_destroy(tc_plan_t p);
+
+/* Profiling: serialised single-stream pass of the plan with CUDA events around
+ * every launch.  Per class c (0 bulk update, 1 last update, 2 POTRF, 3 TRSM,
+ * 4 tree combine, 5 logdet, 6 split-K chunk; n_cls >= 7): summed ms, launch
+ * count and algorithmic flops.  Factorises storage_dev in place. */
+int tc_plan_profile(tc_plan_t p, double* storage_dev, void* stream, int32_t n_cls, double* ms,
+                    int64_t* counts, double* flops);
+/* FP64 tensor-pipe (DMMA m8n8k4) throughput microbenchmark, TFLOP/s. */
+int tc_bench_dmma_peak(int64_t iters, int32_t blocks_per_sm, int32_t warps_per_block,
+                       double* tflops);
 
 #ifdef __cplusplus
 }

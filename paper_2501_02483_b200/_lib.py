@@ -51,6 +51,7 @@ SIGNATURES = {
     "tc_structure_stats": (C.c_int, [i64, i64p, i32p, f64, i64p, i64p]),
     "tc_arrowhead_pattern": (C.c_int, [i64, i64, i64, i32, i64p, i32p]),
     "tc_arrowhead_diag": (C.c_int, [i64, i64p, i32p, f64p]),
+    "tc_band_arrow_pattern": (C.c_int, [i64, i64, i64p, i64p, i32p]),
     "tc_rcm": (C.c_int, [i64, i64p, i32p, i64, i64p]),
     "tc_adaptable_nd": (C.c_int, [i64, i64, i64, i32, i64p]),
     "tc_symbolic_from_csc": (C.c_int, [i64, i32, i64p, i32p, C.POINTER(vp)]),
@@ -82,6 +83,8 @@ SIGNATURES = {
     "tc_plan_pack_offsets": (C.c_int, [vp, i64, i64p, i32p, i64p]),
     "tc_plan_pack": (C.c_int, [vp, vp, vp, i64, vp, vp]),
     "tc_plan_destroy": (None, [vp]),
+    "tc_plan_profile": (C.c_int, [vp, vp, vp, i32, f64p, i64p, f64p]),
+    "tc_bench_dmma_peak": (C.c_int, [i64, i32, i32, f64p]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

@@ -452,6 +452,8 @@ struct Launch {
     int64_t slot = -1;           // POTRF slot / TRSM L slot / COMBINE target
     int64_t scratch0 = 0;        // COMBINE
     uint32_t live = 0;           // COMBINE
+    int cls = 0;                 // profiling class: 0 bulk, 1 last, 2 potrf, 3 trsm, 4 combine, 5 logdet, 6 split-K chunk
+    double flops = 0.0;          // algorithmic flops of this launch
     std::vector<int32_t> deps;
 };
 
@@ -604,7 +606,6 @@ int build_plan(tc_plan& P) {
     std::vector<int32_t> pnode(T, -1);           // launch finishing column k
     std::vector<uint32_t> live_mask(S, 0);
     std::vector<std::vector<int32_t>> buf_writer(S);  // per reduced target: last chunk launch per residue
-    double flops = 0.0;
     const double n3 = (double)nt * nt * nt;
 
     auto add_panel_deps = [&](std::vector<int32_t>& deps, std::vector<int32_t>& cols) {
@@ -639,7 +640,7 @@ int build_plan(tc_plan& P) {
                 if (p1 > tp0[t]) {
                     emit_items(t, tp0[t], p1, (int32_t)t, MODE_SUB);
                     for (int64_t x = tp0[t]; x < p1; ++x) cols.push_back(P.fcol[P.pairs[x].b]);
-                    flops += (P.frow[t] == k ? 1.0 : 2.0) * n3 * (double)(p1 - tp0[t]);
+                    L.flops += (P.frow[t] == k ? 1.0 : 2.0) * n3 * (double)(p1 - tp0[t]);
                 }
             }
             L.cnt = (int64_t)P.items.size() - L.off;
@@ -653,13 +654,14 @@ int build_plan(tc_plan& P) {
             Launch L;
             L.kind = L_UPD;
             L.high = 1;
+            L.cls = 1;
             L.off = (int64_t)P.items.size();
             for (int64_t t = c0; t < c1; ++t) {
                 if (red_base[t] >= 0) continue;
                 const int64_t p1 = tp1[t];
                 if (p1 > tp0[t] && P.fcol[P.pairs[p1 - 1].b] == nlast) {
                     emit_items(t, p1 - 1, p1, (int32_t)t, MODE_SUB);
-                    flops += (P.frow[t] == k ? 1.0 : 2.0) * n3;
+                    L.flops += (P.frow[t] == k ? 1.0 : 2.0) * n3;
                 }
             }
             L.cnt = (int64_t)P.items.size() - L.off;
@@ -677,6 +679,7 @@ int build_plan(tc_plan& P) {
             Launch L;
             L.kind = L_COMBINE;
             L.high = 1;
+            L.cls = 4;
             L.slot = t;
             L.scratch0 = S + red_base[t];
             L.live = live_mask[t];
@@ -692,6 +695,7 @@ int build_plan(tc_plan& P) {
             Launch L;
             L.kind = L_POTRF;
             L.high = 1;
+            L.cls = 2;
             L.k = k;
             L.slot = c0;
             if (bnode >= 0) L.deps.push_back(bnode);
@@ -699,13 +703,14 @@ int build_plan(tc_plan& P) {
             for (int32_t x : comb_diag) L.deps.push_back(x);
             pot = (int32_t)P.launches.size();
             P.launches.push_back(std::move(L));
-            flops += n3 / 3.0;
+            L.flops += n3 / 3.0;
         }
         pnode[k] = pot;
         if (c1 - c0 > 1) {
             Launch L;
             L.kind = L_TRSM;
             L.high = 1;
+            L.cls = 3;
             L.k = k;
             L.slot = c0;
             L.off = (int64_t)P.tgts.size();
@@ -717,7 +722,7 @@ int build_plan(tc_plan& P) {
             for (int32_t x : comb_off) L.deps.push_back(x);
             pnode[k] = (int32_t)P.launches.size();
             P.launches.push_back(std::move(L));
-            flops += n3 * (double)(c1 - c0 - 1);
+            L.flops += n3 * (double)(c1 - c0 - 1);
         }
         // split-K pieces of reduced chains that became ready with column k
         auto& pcs = pieces_at[k];
@@ -728,6 +733,7 @@ int build_plan(tc_plan& P) {
             const int w = pcs[u].j % W;
             Launch L;
             L.kind = L_UPD;
+            L.cls = 6;
             L.off = (int64_t)P.items.size();
             std::vector<int32_t> cols;
             for (size_t z = u; z < v; ++z) {
@@ -739,7 +745,7 @@ int build_plan(tc_plan& P) {
                 live_mask[t] |= 1u << w;
                 for (int64_t x = pc.a; x < pc.b; ++x) cols.push_back(P.fcol[P.pairs[x].b]);
                 if (buf_writer[t][w] >= 0) L.deps.push_back(buf_writer[t][w]);
-                flops += (P.frow[t] == P.fcol[t] ? 1.0 : 2.0) * n3 * (double)(pc.b - pc.a);
+                L.flops += (P.frow[t] == P.fcol[t] ? 1.0 : 2.0) * n3 * (double)(pc.b - pc.a);
             }
             L.cnt = (int64_t)P.items.size() - L.off;
             add_panel_deps(L.deps, cols);
@@ -757,6 +763,7 @@ int build_plan(tc_plan& P) {
         Launch L;
         L.kind = L_LOGDET;
         L.high = 1;
+        L.cls = 5;
         for (size_t i = 0; i < P.launches.size(); ++i)
             if (!has_succ[i]) L.deps.push_back((int32_t)i);
         P.launches.push_back(std::move(L));
@@ -765,7 +772,8 @@ int build_plan(tc_plan& P) {
         std::sort(L.deps.begin(), L.deps.end());
         L.deps.erase(std::unique(L.deps.begin(), L.deps.end()), L.deps.end());
     }
-    P.flops = flops;
+    P.flops = 0.0;
+    for (auto& L : P.launches) P.flops += L.flops;
     // solve metadata
     P.sol_off.assign(T + 1, 0);
     std::vector<int32_t> sslots, srows;
@@ -1160,4 +1168,101 @@ extern "C" void tc_plan_destroy(tc_plan_t p) {
 extern "C" int tc__set_error(int code, const char* msg) {
     g_err = msg;
     return code;
+}
+
+// ---------------------------------------------------------------- profiling --
+// Serialised pass of the plan on one stream with CUDA events around every
+// launch; per profiling class: total ms, launch count, algorithmic flops.
+extern "C" int tc_plan_profile(tc_plan_t p, double* storage, void* stream, int32_t n_cls, double* ms,
+                               int64_t* counts, double* flops) {
+    if (!p || !storage || n_cls < 7 || !ms || !counts || !flops) return set_err(TC_ERR_ARG, "plan_profile: bad arguments");
+    int r = ensure_lane(*p, 0);
+    if (r) return r;
+    r = prep_all(*p);
+    if (r) return r;
+    Lane& ln = p->lanes[0];
+    cudaStream_t s = (cudaStream_t)stream;
+    ln.h.storage = storage;
+    ln.h.scratch = ln.d_scratch;
+    ln.h.S = p->S;
+    ln.h.fail = ln.d_fail;
+    ln.h.ld_part = ln.d_ld;
+    ln.h.ld_out = ln.d_ld + p->T;
+    const int64_t nf = kNoFail;
+    CK(cudaMemcpyAsync(ln.d_ctx, &ln.h, sizeof(Ctx), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ln.d_fail, &nf, 8, cudaMemcpyHostToDevice, s));
+    const size_t NL = p->launches.size();
+    std::vector<cudaEvent_t> ev(NL + 1);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(ev[0], s));
+    for (size_t i = 0; i < NL; ++i) {
+        cudaKernelNodeParams kp;
+        NodeArgs na;
+        void* argv[8];
+        r = node_params(*p, ln, i, kp, na, argv);
+        if (r) return r;
+        CK(cudaLaunchKernel(kp.func, kp.gridDim, kp.blockDim, kp.kernelParams, kp.sharedMemBytes, s));
+        CK(cudaEventRecord(ev[i + 1], s));
+    }
+    CK(cudaStreamSynchronize(s));
+    for (int c = 0; c < n_cls; ++c) {
+        ms[c] = 0.0;
+        counts[c] = 0;
+        flops[c] = 0.0;
+    }
+    for (size_t i = 0; i < NL; ++i) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
+        const int c = p->launches[i].cls;
+        ms[c] += t;
+        counts[c] += 1;
+        flops[c] += p->launches[i].flops;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    return TC_OK;
+}
+
+// DMMA throughput microbenchmark: every warp issues independent m8n8k4 FP64
+// MMAs from registers; returns TFLOP/s over the whole device.
+namespace {
+__global__ void k_dmma_peak(int64_t iters, double* sink) {
+    double a = threadIdx.x * 1e-3, b = blockIdx.x * 1e-3;
+    double d[8][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i][0] = d[i][1] = 0.0;
+    for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dmma(d[i][0], d[i][1], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += d[i][0] + d[i][1];
+    if (s == 12345.678) sink[0] = s;
+}
+}  // namespace
+
+extern "C" int tc_bench_dmma_peak(int64_t iters, int32_t blocks_per_sm, int32_t warps_per_block, double* tflops) {
+    if (iters < 1 || !tflops) return set_err(TC_ERR_ARG, "dmma_peak: bad arguments");
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    double* sink = nullptr;
+    CK(cudaMalloc(&sink, 8));
+    const int grid = sms * blocks_per_sm, block = 32 * warps_per_block;
+    k_dmma_peak<<<grid, block>>>(iters / 10 + 1, sink);
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a));
+    k_dmma_peak<<<grid, block>>>(iters, sink);
+    CK(cudaEventRecord(b));
+    CK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    const double fl = 2.0 * 256.0 * 8.0 * (double)iters * grid * warps_per_block;  // 256 FMA per DMMA per warp
+    *tflops = fl / (ms * 1e-3) / 1e12;
+    cudaFree(sink);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return TC_OK;
 }

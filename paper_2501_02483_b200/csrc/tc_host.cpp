@@ -415,6 +415,27 @@ extern "C" int tc_arrowhead_pattern(int64_t n, int64_t b, int64_t t, int32_t bd,
     GUARD_END
 }
 
+extern "C" int tc_band_arrow_pattern(int64_t n, int64_t t, const int64_t* band, int64_t* cp, int32_t* ri) {
+    if (n < 1 || t < 0 || t >= n || !band || !cp) return herr(TC_ERR_ARG, "band_arrow_pattern: bad arguments");
+    GUARD_BEGIN
+    const int64_t nh = n - t;
+    for (int64_t j = 0; j < nh; ++j)
+        if (band[j] < 0 || j + band[j] >= nh) return herr(TC_ERR_ARG, "band_arrow_pattern: band leaves the head block");
+    cp[0] = 0;
+    for (int64_t j = 0; j < n; ++j) cp[j + 1] = cp[j] + (j < nh ? 1 + band[j] + t : n - j);
+    if (ri) {
+        for (int64_t j = 0; j < n; ++j) {
+            int64_t e = cp[j];
+            const int64_t top = j < nh ? j + band[j] : n - 1;
+            for (int64_t r = j; r <= top; ++r) ri[e++] = (int32_t)r;
+            if (j < nh)
+                for (int64_t r = nh; r < n; ++r) ri[e++] = (int32_t)r;
+        }
+    }
+    return TC_OK;
+    GUARD_END
+}
+
 extern "C" int tc_arrowhead_diag(int64_t n, const int64_t* cp, const int32_t* ri, double* v) {
     if (n < 1 || !cp || !ri || !v) return herr(TC_ERR_ARG, "arrowhead_diag: bad arguments");
     GUARD_BEGIN
