@@ -701,9 +701,9 @@ int build_plan(tc_plan& P) {
             if (bnode >= 0) L.deps.push_back(bnode);
             if (lnode >= 0) L.deps.push_back(lnode);
             for (int32_t x : comb_diag) L.deps.push_back(x);
+            L.flops += n3 / 3.0;
             pot = (int32_t)P.launches.size();
             P.launches.push_back(std::move(L));
-            L.flops += n3 / 3.0;
         }
         pnode[k] = pot;
         if (c1 - c0 > 1) {
@@ -720,9 +720,9 @@ int build_plan(tc_plan& P) {
             if (bnode >= 0) L.deps.push_back(bnode);
             if (lnode >= 0) L.deps.push_back(lnode);
             for (int32_t x : comb_off) L.deps.push_back(x);
+            L.flops += n3 * (double)(c1 - c0 - 1);
             pnode[k] = (int32_t)P.launches.size();
             P.launches.push_back(std::move(L));
-            L.flops += n3 * (double)(c1 - c0 - 1);
         }
         // split-K pieces of reduced chains that became ready with column k
         auto& pcs = pieces_at[k];
