@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--measure-peaks", action="store_true")
     ap.add_argument("--ref-procs", type=int, default=0)
+    ap.add_argument("--executor", default="persistent", choices=["persistent", "graph", "direct"])
     return ap.parse_args()
 
 
@@ -297,7 +298,7 @@ def run_ours(a, name, nt, desc, rank, world):
     from paper_2501_02483_b200._lib import check, lib, f64p, i64p
 
     m = build_matrix(name)
-    opts = api.FactorOptions(tile_size=nt)
+    opts = api.FactorOptions(tile_size=nt, executor=a.executor)
     t0 = time.perf_counter()
     pat = api._pattern_for(m, opts)
     setup_s = time.perf_counter() - t0

@@ -47,7 +47,7 @@ class FactorOptions:
     ordering: str = "auto"
     tree_reduction: str = "auto"
     lookahead: bool = True
-    use_graph: bool = True
+    executor: str = "persistent"  # persistent | graph | direct
     chunk: int = 0
 
     def __post_init__(self):
@@ -59,12 +59,14 @@ class FactorOptions:
             raise ValueError(f"unknown ordering policy {self.ordering!r}")
         if self.tree_reduction not in _REDUCTIONS:
             raise ValueError(f"unknown tree_reduction policy {self.tree_reduction!r}")
+        if self.executor not in ("persistent", "graph", "direct"):
+            raise ValueError(f"unknown executor {self.executor!r}")
 
     def plan_options(self) -> PlanOptions:
         W = self.workers if self.workers >= 2 else 8
         thr = -1 if self.tree_reduction == "off" else 0
         return PlanOptions(tree_workers=min(W, 16), tree_threshold=thr, chunk=self.chunk,
-                           lookahead=self.lookahead, use_graph=self.use_graph)
+                           lookahead=self.lookahead, executor=self.executor)
 
 
 @dataclass(eq=False)

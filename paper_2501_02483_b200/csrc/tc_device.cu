@@ -71,6 +71,25 @@ UpdKernel pick_upd(int nt) {
     return mk_upd<32, 32, 2, 2, 1>();
 }
 
+struct PersistKernel {
+    void (*fn)(PersistArgs);
+    int BM, BN, smem;
+};
+
+template <int BM, int BN, int WGM, int WGN, int KS>
+PersistKernel mk_persist() {
+    return PersistKernel{k_persist<BM, BN, WGM, WGN, KS>, BM, BN, UpdCfg<BM, BN, WGM, WGN, KS>::SMEM};
+}
+
+// same block shapes as pick_upd, 256-thread variants (KSPLIT doubled)
+PersistKernel pick_persist(int nt) {
+    if (nt % 80 == 0 && nt % 48 == 0) return mk_persist<80, 48, 2, 2, 2>();
+    if (nt % 80 == 0) return mk_persist<80, 40, 2, 1, 4>();
+    if (nt % 40 == 0) return mk_persist<40, 40, 1, 1, 8>();
+    if (nt >= 96) return mk_persist<64, 64, 2, 2, 2>();
+    return mk_persist<32, 32, 2, 2, 2>();
+}
+
 int prep_kernel(const void* fn, int smem) {
     if (smem > 48 * 1024) {
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -464,6 +483,7 @@ struct Lane {
     double* d_scratch = nullptr;
     cudaGraphExec_t exec = nullptr;
     cudaGraph_t graph = nullptr;
+    int32_t* d_pstate = nullptr;  // persistent: [remaining | deps_left | ticket]
     Ctx h{};
 };
 
@@ -497,6 +517,20 @@ struct tc_plan {
     std::vector<Lane> lanes;
     int prio_hi = 0, prio_lo = 0;
     int dev = 0;
+    // per-column launch ids (persistent ticket order)
+    std::vector<int32_t> colB, colL, colPot, colTrsm;
+    std::vector<std::vector<int32_t>> colComb, colChunk;
+    // persistent executor
+    std::vector<PTask> ptasks;
+    std::vector<PLaunch> plaunch;
+    std::vector<int32_t> p_remaining, p_deps, p_succ_ptr, p_succ;
+    PTask* d_ptasks = nullptr;
+    PLaunch* d_plaunch = nullptr;
+    int32_t* d_p_init = nullptr;  // [remaining | deps_left] pristine copy
+    int32_t* d_succ_ptr = nullptr;
+    int32_t* d_succ = nullptr;
+    size_t persist_smem = 0;
+    int persist_grid = 0;
 };
 
 namespace {
@@ -508,6 +542,8 @@ int64_t find_slot(const tc_plan& P, int32_t m, int32_t c) {
     const int32_t* it = std::lower_bound(b, e, m);
     return (it != e && *it == m) ? (int64_t)(it - P.frow.data()) : -1;
 }
+
+int build_persistent(tc_plan& P);
 
 int build_plan(tc_plan& P) {
     const int T = P.T, nt = P.nt;
@@ -601,6 +637,12 @@ int build_plan(tc_plan& P) {
 
     // ---- pass 2: launches in topological order
     P.launches.clear();
+    P.colB.assign(T, -1);
+    P.colL.assign(T, -1);
+    P.colPot.assign(T, -1);
+    P.colTrsm.assign(T, -1);
+    P.colComb.assign(T, {});
+    P.colChunk.assign(T, {});
     P.items.clear();
     P.tgts.clear();
     std::vector<int32_t> pnode(T, -1);           // launch finishing column k
@@ -647,6 +689,7 @@ int build_plan(tc_plan& P) {
             if (L.cnt > 0) {
                 add_panel_deps(L.deps, cols);
                 bnode = (int32_t)P.launches.size();
+                P.colB[k] = bnode;
                 P.launches.push_back(std::move(L));
             }
         }
@@ -669,6 +712,7 @@ int build_plan(tc_plan& P) {
                 L.deps.push_back(pnode[nlast]);
                 if (bnode >= 0) L.deps.push_back(bnode);
                 lnode = (int32_t)P.launches.size();
+                P.colL[k] = lnode;
                 P.launches.push_back(std::move(L));
             }
         }
@@ -687,6 +731,7 @@ int build_plan(tc_plan& P) {
                 if (w >= 0) L.deps.push_back(w);
             const int32_t id = (int32_t)P.launches.size();
             (P.frow[t] == k ? comb_diag : comb_off).push_back(id);
+            P.colComb[k].push_back(id);
             P.launches.push_back(std::move(L));
         }
         // POTRF(k)
@@ -703,6 +748,7 @@ int build_plan(tc_plan& P) {
             for (int32_t x : comb_diag) L.deps.push_back(x);
             L.flops += n3 / 3.0;
             pot = (int32_t)P.launches.size();
+            P.colPot[k] = pot;
             P.launches.push_back(std::move(L));
         }
         pnode[k] = pot;
@@ -722,6 +768,7 @@ int build_plan(tc_plan& P) {
             for (int32_t x : comb_off) L.deps.push_back(x);
             L.flops += n3 * (double)(c1 - c0 - 1);
             pnode[k] = (int32_t)P.launches.size();
+            P.colTrsm[k] = pnode[k];
             P.launches.push_back(std::move(L));
         }
         // split-K pieces of reduced chains that became ready with column k
@@ -751,6 +798,7 @@ int build_plan(tc_plan& P) {
             add_panel_deps(L.deps, cols);
             const int32_t id = (int32_t)P.launches.size();
             for (size_t z = u; z < v; ++z) buf_writer[pcs[z].t][w] = id;
+            P.colChunk[k].push_back(id);
             P.launches.push_back(std::move(L));
             u = v;
         }
@@ -795,6 +843,158 @@ int build_plan(tc_plan& P) {
     if (!r) r = upload(srows, &P.d_sol_rows, s);
     if (r) return r;
     CK(cudaStreamSynchronize(s));
+    if (P.opts.use_graph == 2 && (nt & 1) == 0) return build_persistent(P);
+    if (P.opts.use_graph == 2) P.opts.use_graph = 1;  // odd nt: 8-byte copies go through L1 -> graph mode
+    return TC_OK;
+}
+
+// Ticket order + flat task list of the persistent executor.  Per column k:
+// L(k), combines(k), POTRF(k), B(k+1), TRSM(k), split-K chunks ready at k —
+// the bulk update of the next column is handed out before the TRSM tiles of
+// this one so CTAs have work while POTRF(k) runs.  Falls back to creation
+// order (always topological) if the heuristic order were not.
+int build_persistent(tc_plan& P) {
+    const int T = P.T, nt = P.nt;
+    const size_t NL = P.launches.size();
+    std::vector<int32_t> order;
+    order.reserve(NL);
+    std::vector<char> placed(NL, 0);
+    auto put = [&](int32_t id) {
+        if (id >= 0 && !placed[id]) {
+            placed[id] = 1;
+            order.push_back(id);
+        }
+    };
+    if (T > 0) put(P.colB[0]);
+    for (int k = 0; k < T; ++k) {
+        put(P.colL[k]);
+        for (int32_t c : P.colComb[k]) put(c);
+        put(P.colPot[k]);
+        if (k + 1 < T) put(P.colB[k + 1]);
+        put(P.colTrsm[k]);
+        for (int32_t c : P.colChunk[k]) put(c);
+    }
+    for (size_t i = 0; i < NL; ++i) put((int32_t)i);
+    std::vector<int32_t> pos(NL);
+    for (size_t i = 0; i < NL; ++i) pos[order[i]] = (int32_t)i;
+    bool topo = true;
+    for (size_t i = 0; i < NL && topo; ++i)
+        for (int32_t d : P.launches[i].deps)
+            if (pos[d] >= pos[i]) {
+                topo = false;
+                break;
+            }
+    if (!topo)
+        for (size_t i = 0; i < NL; ++i) order[i] = (int32_t)i;
+    P.ptasks.clear();
+    P.p_remaining.assign(NL, 0);
+    P.p_deps.assign(NL, 0);
+    const int nrb = (nt + kPersistTrsmRows - 1) / kPersistTrsmRows;
+    for (int32_t id : order) {
+        const Launch& L = P.launches[id];
+        const size_t before = P.ptasks.size();
+        switch (L.kind) {
+            case L_UPD:
+                for (int64_t x = L.off; x < L.off + L.cnt; ++x) P.ptasks.push_back(PTask{id, (int32_t)x, 0});
+                break;
+            case L_TRSM:
+                for (int64_t x = L.off; x < L.off + L.cnt; ++x)
+                    for (int rb = 0; rb < nrb; ++rb) P.ptasks.push_back(PTask{id, P.tgts[x], rb});
+                break;
+            default:
+                P.ptasks.push_back(PTask{id, 0, 0});
+                break;
+        }
+        P.p_remaining[id] = (int32_t)(P.ptasks.size() - before);
+        P.p_deps[id] = (int32_t)L.deps.size();
+    }
+    if (P.ptasks.size() > (size_t)INT32_MAX / 2) return set_err(TC_ERR_ARG, "plan: too many tasks");
+    P.p_succ_ptr.assign(NL + 1, 0);
+    for (size_t i = 0; i < NL; ++i)
+        for (int32_t d : P.launches[i].deps) P.p_succ_ptr[d + 1]++;
+    for (size_t i = 0; i < NL; ++i) P.p_succ_ptr[i + 1] += P.p_succ_ptr[i];
+    P.p_succ.assign(P.p_succ_ptr[NL], 0);
+    {
+        std::vector<int32_t> at(P.p_succ_ptr.begin(), P.p_succ_ptr.end() - 1);
+        for (size_t i = 0; i < NL; ++i)
+            for (int32_t d : P.launches[i].deps) P.p_succ[at[d]++] = (int32_t)i;
+    }
+    P.plaunch.assign(NL, PLaunch{});
+    for (size_t i = 0; i < NL; ++i) {
+        const Launch& L = P.launches[i];
+        PLaunch& q = P.plaunch[i];
+        switch (L.kind) {
+            case L_UPD: q.kind = 0; break;
+            case L_POTRF:
+                q.kind = 1;
+                q.k = L.k;
+                q.slot = L.slot;
+                q.live = (int32_t)std::min<int64_t>(P.n - (int64_t)L.k * nt, nt);
+                break;
+            case L_TRSM:
+                q.kind = 2;
+                q.k = L.k;
+                q.slot = L.slot;
+                break;
+            case L_COMBINE:
+                q.kind = 3;
+                q.slot = L.slot;
+                q.scratch0 = L.scratch0 - P.S;
+                q.live = (int32_t)L.live;
+                break;
+            default: q.kind = 4; break;
+        }
+    }
+    std::vector<int32_t> init(P.p_remaining);
+    init.insert(init.end(), P.p_deps.begin(), P.p_deps.end());
+    cudaStream_t s0 = 0;
+    int r = upload(P.ptasks, &P.d_ptasks, s0);
+    if (!r) r = upload(P.plaunch, &P.d_plaunch, s0);
+    if (!r) r = upload(init, &P.d_p_init, s0);
+    if (!r) r = upload(P.p_succ_ptr, &P.d_succ_ptr, s0);
+    if (!r) r = upload(P.p_succ, &P.d_succ, s0);
+    if (r) return r;
+    const PersistKernel K = pick_persist(nt);
+    bool in_smem;
+    P.persist_smem = std::max<size_t>({(size_t)K.smem, potrf_smem(nt, &in_smem), trsm_smem_bytes<kPersistTrsmRows>(nt),
+                                       (size_t)4096});
+    r = prep_kernel((const void*)K.fn, (int)P.persist_smem);
+    if (r) return r;
+    int per_sm = 0, sms = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K.fn, kPersistThreads, P.persist_smem));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P.dev));
+    if (per_sm < 1) return set_err(TC_ERR_CUDA, "persistent kernel does not fit on an SM (smem %zu)", P.persist_smem);
+    P.persist_grid = per_sm * sms;
+    CK(cudaStreamSynchronize(s0));
+    return TC_OK;
+}
+
+int run_persistent(tc_plan& P, Lane& ln, cudaStream_t s) {
+    const size_t NL = P.launches.size();
+    if (!ln.d_pstate) CK(cudaMalloc(&ln.d_pstate, (2 * NL + 1) * sizeof(int32_t)));
+    CK(cudaMemcpyAsync(ln.d_pstate, P.d_p_init, 2 * NL * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemsetAsync(ln.d_pstate + 2 * NL, 0, sizeof(int32_t), s));
+    PersistArgs a{};
+    a.ctx = ln.d_ctx;
+    a.items = P.d_items;
+    a.pairs = P.d_pairs;
+    a.tasks = P.d_ptasks;
+    a.launches = P.d_plaunch;
+    a.ntasks = (int32_t)P.ptasks.size();
+    a.remaining = ln.d_pstate;
+    a.deps_left = ln.d_pstate + NL;
+    a.succ_ptr = P.d_succ_ptr;
+    a.succ = P.d_succ;
+    a.ticket = ln.d_pstate + 2 * NL;
+    a.nt = P.nt;
+    a.W = P.W;
+    a.T = P.T;
+    bool in_smem;
+    potrf_smem(P.nt, &in_smem);
+    a.potrf_in_smem = in_smem;
+    const PersistKernel K = pick_persist(P.nt);
+    K.fn<<<P.persist_grid, kPersistThreads, P.persist_smem, s>>>(a);
+    CK(cudaGetLastError());
     return TC_OK;
 }
 
@@ -984,7 +1184,7 @@ extern "C" int tc_plan_create(int64_t n, int32_t nt, int64_t S, const int32_t* f
     else {
         memset(&P->opts, 0, sizeof P->opts);
         P->opts.lookahead = 1;
-        P->opts.use_graph = 1;
+        P->opts.use_graph = 2;
     }
     P->W = P->opts.tree_workers > 0 ? P->opts.tree_workers : 8;
     if (P->W > kMaxW) return set_err(TC_ERR_ARG, "plan_create: tree_workers <= %d", kMaxW);
@@ -1029,7 +1229,10 @@ extern "C" int tc_plan_factorize_async(tc_plan_t p, int32_t lane, double* storag
     const int64_t nf = kNoFail;
     CK(cudaMemcpyAsync(ln.d_ctx, &ln.h, sizeof(Ctx), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(ln.d_fail, &nf, 8, cudaMemcpyHostToDevice, s));
-    if (p->opts.use_graph) {
+    if (p->opts.use_graph == 2) {
+        r = run_persistent(*p, ln, s);
+        if (r) return r;
+    } else if (p->opts.use_graph) {
         r = build_graph(*p, ln);
         if (r) return r;
         CK(cudaGraphLaunch(ln.exec, s));
@@ -1154,7 +1357,13 @@ extern "C" void tc_plan_destroy(tc_plan_t p) {
         cudaFree(ln.d_fail);
         cudaFree(ln.d_ld);
         cudaFree(ln.d_scratch);
+        cudaFree(ln.d_pstate);
     }
+    cudaFree(p->d_ptasks);
+    cudaFree(p->d_plaunch);
+    cudaFree(p->d_p_init);
+    cudaFree(p->d_succ_ptr);
+    cudaFree(p->d_succ);
     cudaFree(p->d_items);
     cudaFree(p->d_pairs);
     cudaFree(p->d_tgts);

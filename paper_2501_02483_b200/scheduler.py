@@ -8,8 +8,11 @@ The plan is built once per factor tile pattern in C++ (``tc_plan_create``):
 * chains with accum >= 2W (the arrow x arrow tiles) are split-K over W
   partial tiles filled as the band factorisation proceeds and combined by the
   deterministic pairwise tree of symbolic._combine_steps (Alg. 3);
-* the launches form a dependency DAG executed as one CUDA graph per lane
-  with critical-path nodes at high stream priority.
+* the launches form a dependency DAG, executed either by the persistent
+  dataflow kernel (default: one launch, tasks handed out by a device ticket
+  counter in a topological priority order, per-launch dependency counters —
+  the device form of the paper's progress table) or as one CUDA graph per
+  lane with critical-path nodes at high stream priority.
 
 ``compile_ops`` (the reference-compatible op stream for ``run_ops``) lives in
 symbolic.py.
@@ -35,7 +38,7 @@ class PlanOptions:
     tree_threshold: int = 0      # 0 = 2*W (reference rule), < 0 = no tree reduction
     chunk: int = 0               # columns per split-K launch (0 = 8)
     lookahead: bool = True
-    use_graph: bool = True
+    executor: str = "persistent"  # persistent | graph | direct
 
     def to_c(self) -> PlanOpts:
         o = PlanOpts()
@@ -43,7 +46,7 @@ class PlanOptions:
         o.tree_threshold = self.tree_threshold
         o.chunk = self.chunk
         o.lookahead = int(self.lookahead)
-        o.use_graph = int(self.use_graph)
+        o.use_graph = {"direct": 0, "graph": 1, "persistent": 2}[self.executor]
         return o
 
 

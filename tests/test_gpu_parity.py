@@ -204,7 +204,7 @@ def test_factorize_plan_path(torch, name):
 
 
 @pytest.mark.parametrize("variant", [
-    dict(tree_reduction="off"), dict(lookahead=False), dict(use_graph=False),
+    dict(tree_reduction="off"), dict(lookahead=False), dict(executor="direct"), dict(executor="graph"),
     dict(workers=2), dict(workers=4, chunk=3), dict(workers=16, chunk=1)])
 def test_factorize_plan_variants(torch, variant):
     api, ctsf, matcore, symbolic, impl = _imports()
@@ -221,8 +221,9 @@ def test_graph_and_direct_bitwise_and_batch_isolation(torch):
     m = _pm(z)
     nt = int(z["nt"])
     a = api.factorize(m, api.FactorOptions(tile_size=nt)).factor.host_storage()
-    b = api.factorize(m, api.FactorOptions(tile_size=nt, use_graph=False)).factor.host_storage()
-    assert np.array_equal(a, b)  # deterministic: same kernels, fixed orders
+    b = api.factorize(m, api.FactorOptions(tile_size=nt, executor="direct")).factor.host_storage()
+    c = api.factorize(m, api.FactorOptions(tile_size=nt, executor="graph")).factor.host_storage()
+    assert np.array_equal(a, b) and np.array_equal(a, c)  # deterministic: fixed orders, no data atomics
     ms = []
     for seed in range(5):
         v = m.values * (1.0 + 0.01 * seed)

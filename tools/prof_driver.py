@@ -14,10 +14,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="c2")
 ap.add_argument("--tile", type=int, default=120)
 ap.add_argument("--reps", type=int, default=1)
-ap.add_argument("--direct", action="store_true")
+ap.add_argument("--executor", default="persistent")
 a = ap.parse_args()
 m = bench.build_matrix(a.workload)
-opts = api.FactorOptions(tile_size=a.tile, use_graph=not a.direct)
+opts = api.FactorOptions(tile_size=a.tile, executor=a.executor)
 pat = api._pattern_for(m, opts)
 plan = pat.plan
 vals = torch.from_numpy(np.ascontiguousarray(pat.permuted_values(m))).cuda()
