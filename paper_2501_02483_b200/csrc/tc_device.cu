@@ -484,6 +484,7 @@ struct Lane {
     cudaGraphExec_t exec = nullptr;
     cudaGraph_t graph = nullptr;
     int32_t* d_pstate = nullptr;  // persistent: [remaining | deps_left | ticket]
+    int32_t* d_prog = nullptr;    // persistent fused: per-column POTRF panel progress [T]
     Ctx h{};
 };
 
@@ -530,6 +531,7 @@ struct tc_plan {
     int32_t* d_succ_ptr = nullptr;
     int32_t* d_succ = nullptr;
     size_t persist_smem = 0;
+    bool fuse = true;  // persistent executor: TRSM(k) streams POTRF(k)'s panels
     int persist_grid = 0;
 };
 
@@ -865,11 +867,28 @@ int build_persistent(tc_plan& P) {
             order.push_back(id);
         }
     };
+    // Fused POTRF -> TRSM: TRSM(k) tasks no longer wait for POTRF(k) to end;
+    // they consume its panels through the per-column progress counter, so
+    // they are ticketed right behind it.  The log-det node must then wait
+    // for every POTRF explicitly (its partials are written at POTRF's end).
+    const bool fuse = P.fuse;
+    std::vector<std::vector<int32_t>> pdeps(NL);
+    for (size_t i = 0; i < NL; ++i) {
+        const Launch& L = P.launches[i];
+        for (int32_t d : L.deps)
+            if (!(fuse && L.kind == L_TRSM && P.launches[d].kind == L_POTRF && P.launches[d].k == L.k))
+                pdeps[i].push_back(d);
+        if (fuse && L.kind == L_LOGDET)
+            for (int k = 0; k < T; ++k) pdeps[i].push_back(P.colPot[k]);
+        std::sort(pdeps[i].begin(), pdeps[i].end());
+        pdeps[i].erase(std::unique(pdeps[i].begin(), pdeps[i].end()), pdeps[i].end());
+    }
     if (T > 0) put(P.colB[0]);
     for (int k = 0; k < T; ++k) {
         put(P.colL[k]);
         for (int32_t c : P.colComb[k]) put(c);
         put(P.colPot[k]);
+        if (fuse) put(P.colTrsm[k]);
         if (k + 1 < T) put(P.colB[k + 1]);
         put(P.colTrsm[k]);
         for (int32_t c : P.colChunk[k]) put(c);
@@ -879,7 +898,7 @@ int build_persistent(tc_plan& P) {
     for (size_t i = 0; i < NL; ++i) pos[order[i]] = (int32_t)i;
     bool topo = true;
     for (size_t i = 0; i < NL && topo; ++i)
-        for (int32_t d : P.launches[i].deps)
+        for (int32_t d : pdeps[i])
             if (pos[d] >= pos[i]) {
                 topo = false;
                 break;
@@ -906,18 +925,18 @@ int build_persistent(tc_plan& P) {
                 break;
         }
         P.p_remaining[id] = (int32_t)(P.ptasks.size() - before);
-        P.p_deps[id] = (int32_t)L.deps.size();
+        P.p_deps[id] = (int32_t)pdeps[id].size();
     }
     if (P.ptasks.size() > (size_t)INT32_MAX / 2) return set_err(TC_ERR_ARG, "plan: too many tasks");
     P.p_succ_ptr.assign(NL + 1, 0);
     for (size_t i = 0; i < NL; ++i)
-        for (int32_t d : P.launches[i].deps) P.p_succ_ptr[d + 1]++;
+        for (int32_t d : pdeps[i]) P.p_succ_ptr[d + 1]++;
     for (size_t i = 0; i < NL; ++i) P.p_succ_ptr[i + 1] += P.p_succ_ptr[i];
     P.p_succ.assign(P.p_succ_ptr[NL], 0);
     {
         std::vector<int32_t> at(P.p_succ_ptr.begin(), P.p_succ_ptr.end() - 1);
         for (size_t i = 0; i < NL; ++i)
-            for (int32_t d : P.launches[i].deps) P.p_succ[at[d]++] = (int32_t)i;
+            for (int32_t d : pdeps[i]) P.p_succ[at[d]++] = (int32_t)i;
     }
     P.plaunch.assign(NL, PLaunch{});
     for (size_t i = 0; i < NL; ++i) {
@@ -974,6 +993,10 @@ int run_persistent(tc_plan& P, Lane& ln, cudaStream_t s) {
     if (!ln.d_pstate) CK(cudaMalloc(&ln.d_pstate, (2 * NL + 1) * sizeof(int32_t)));
     CK(cudaMemcpyAsync(ln.d_pstate, P.d_p_init, 2 * NL * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     CK(cudaMemsetAsync(ln.d_pstate + 2 * NL, 0, sizeof(int32_t), s));
+    if (P.fuse) {
+        if (!ln.d_prog) CK(cudaMalloc(&ln.d_prog, (size_t)P.T * sizeof(int32_t)));
+        CK(cudaMemsetAsync(ln.d_prog, 0, (size_t)P.T * sizeof(int32_t), s));
+    }
     PersistArgs a{};
     a.ctx = ln.d_ctx;
     a.items = P.d_items;
@@ -992,6 +1015,7 @@ int run_persistent(tc_plan& P, Lane& ln, cudaStream_t s) {
     bool in_smem;
     potrf_smem(P.nt, &in_smem);
     a.potrf_in_smem = in_smem;
+    a.prog = P.fuse ? ln.d_prog : nullptr;
     const PersistKernel K = pick_persist(P.nt);
     K.fn<<<P.persist_grid, kPersistThreads, P.persist_smem, s>>>(a);
     CK(cudaGetLastError());
@@ -1187,6 +1211,7 @@ extern "C" int tc_plan_create(int64_t n, int32_t nt, int64_t S, const int32_t* f
         P->opts.use_graph = 2;
     }
     P->W = P->opts.tree_workers > 0 ? P->opts.tree_workers : 8;
+    P->fuse = P->opts.reserved[0] == 0;  // reserved[0] = 1 disables POTRF->TRSM streaming
     if (P->W > kMaxW) return set_err(TC_ERR_ARG, "plan_create: tree_workers <= %d", kMaxW);
     if (P->opts.tree_threshold == 0) P->opts.tree_threshold = 2 * P->W;
     P->frow.assign(f_rows, f_rows + S);
@@ -1358,6 +1383,7 @@ extern "C" void tc_plan_destroy(tc_plan_t p) {
         cudaFree(ln.d_ld);
         cudaFree(ln.d_scratch);
         cudaFree(ln.d_pstate);
+        cudaFree(ln.d_prog);
     }
     cudaFree(p->d_ptasks);
     cudaFree(p->d_plaunch);

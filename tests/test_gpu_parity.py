@@ -220,10 +220,15 @@ def test_graph_and_direct_bitwise_and_batch_isolation(torch):
     z = load_case("d1000")
     m = _pm(z)
     nt = int(z["nt"])
+    # deterministic: fixed summation orders, no atomics on data.  Graph and
+    # direct launch the same kernels; the persistent executor uses 256-thread
+    # update variants (different split-K reduction order) -> equal within FP.
     a = api.factorize(m, api.FactorOptions(tile_size=nt)).factor.host_storage()
+    a2 = api.factorize(m, api.FactorOptions(tile_size=nt)).factor.host_storage()
     b = api.factorize(m, api.FactorOptions(tile_size=nt, executor="direct")).factor.host_storage()
     c = api.factorize(m, api.FactorOptions(tile_size=nt, executor="graph")).factor.host_storage()
-    assert np.array_equal(a, b) and np.array_equal(a, c)  # deterministic: fixed orders, no data atomics
+    assert np.array_equal(a, a2) and np.array_equal(b, c)
+    assert relf(a, b) < FACTOR_TOL
     ms = []
     for seed in range(5):
         v = m.values * (1.0 + 0.01 * seed)
