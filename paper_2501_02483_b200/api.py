@@ -314,34 +314,22 @@ def factorize_many_sharded(problems, rhs=None, opts: FactorOptions | None = None
     ``rhs`` when given) are exchanged — one all-gather over NVLink.
 
     Returns {"logdet": float64[P], "x": list of arrays or None, "local": local results}."""
-    import torch
     import torch.distributed as dist
+    from .batch import gather_rows, shard_range
     P = len(problems)
     world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank(group) if world > 1 else 0
-    lo, hi = (rank * P) // world, ((rank + 1) * P) // world
+    lo, hi = shard_range(P, world, rank)
     local = factorize_many(problems[lo:hi], opts=opts, lanes=lanes) if hi > lo else []
     n = problems[0].n if isinstance(problems[0], SymmetricCsc) else problems[0][0].n
-    per = (hi - lo)
     width = 1 + (n if (rhs is not None and return_solutions) else 0)
-    cap = -(-P // world)
-    buf = torch.zeros((cap, width), dtype=torch.float64, device="cuda")
+    rows = np.zeros((hi - lo, width))
     for j, ctx in enumerate(local):
-        buf[j, 0] = logdet(ctx)
+        rows[j, 0] = logdet(ctx)
         if width > 1:
             b = rhs[lo + j] if isinstance(rhs, (list, tuple)) else rhs
-            buf[j, 1:] = torch.from_numpy(solve(ctx, b)).cuda()
-    if world > 1:
-        out = [torch.empty_like(buf) for _ in range(world)]
-        dist.all_gather(out, buf, group=group)
-    else:
-        out = [buf]
-    gathered = []
-    for r in range(world):
-        a, b = (r * P) // world, ((r + 1) * P) // world
-        gathered.append(out[r][: b - a])
-    allv = torch.cat(gathered).cpu().numpy()
-    del per
+            rows[j, 1:] = solve(ctx, b)
+    allv = gather_rows(rows, P, group=group, device="cuda")
     return {"logdet": allv[:, 0].copy(),
             "x": [allv[i, 1:].copy() for i in range(P)] if width > 1 else None,
             "local": local}

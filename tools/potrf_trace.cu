@@ -21,6 +21,7 @@ int main() {
         int NB = ntp / 8;
         long long t0 = t[0];
         printf("nt=%d: per panel [gemm_start gemm_end chol_done trsm(K+1)_done] rel cycles\n", nt);
-        for (int K = 0; K < NB; ++K) printf("  K=%2d %7lld %7lld %7lld %7lld\n", K, t[4*K]-t0, t[4*K+1]-t0, t[4*K+2]-t0, (K+1<NB)? t[4*K+3]-t0 : 0);
+        for (int K = 0; K < NB; ++K) printf("  K=%2d %7lld %7lld %7lld %7lld | next-owner: gemm_done %7lld diag_seen %7lld solved %7lld\n", K, t[4*K]-t0, t[4*K+1]-t0, t[4*K+2]-t0, (K+1<NB)? t[4*K+3]-t0 : 0,
+            (K+1<NB)? t[1000+4*K]-t0:0, (K+1<NB)? t[1000+4*K+1]-t0:0, (K+1<NB)? t[1000+4*K+2]-t0:0);
     }
 }
