@@ -31,7 +31,7 @@ sys.path.insert(0, ROOT)
 
 WORKLOADS = {
     "c1": ("arrowhead n=10,000 b=200 t=50 (BASELINE config 1)", 120),
-    "c2": ("variable-band arrowhead n=100,000 max band 1,000 t=200 (BASELINE config 2)", 240),
+    "c2": ("variable-band arrowhead n=100,000 max band 1,000 t=200 (BASELINE config 2)", 120),
     "c3": ("INLA 2000x100+10 (n=200,010) kappa=.5 rho=.9 tau=1e-3 (BASELINE config 3)", 240),
     "c4": ("arrowhead n=1,000,000 b=2000 t=500 (BASELINE config 4)", 240),
 }
@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--measure-peaks", action="store_true")
     ap.add_argument("--ref-procs", type=int, default=0)
     ap.add_argument("--executor", default="persistent", choices=["persistent", "graph", "direct"])
+    ap.add_argument("--ordering", default="auto",
+                    help="auto (SPEC policy) | identity (C4: auto provably picks identity, zero fill)")
     return ap.parse_args()
 
 
@@ -298,7 +300,7 @@ def run_ours(a, name, nt, desc, rank, world):
     from paper_2501_02483_b200._lib import check, lib, f64p, i64p
 
     m = build_matrix(name)
-    opts = api.FactorOptions(tile_size=nt, executor=a.executor)
+    opts = api.FactorOptions(tile_size=nt, executor=a.executor, ordering=a.ordering)
     t0 = time.perf_counter()
     pat = api._pattern_for(m, opts)
     setup_s = time.perf_counter() - t0
