@@ -426,12 +426,11 @@ def run_ours(a, name, nt, desc, rank, world):
 
 
 def _useful_flops(pat):
-    try:
-        cp = pat.pm_pattern.col_ptr
-        # sum_j c_j^2 with c_j = column counts of L: use the exact fill count per column
-        return None if cp is None else None
-    except Exception:  # noqa: BLE001
-        return None
+    """sum_j c_j^2 over the scalar factor's column counts (tile-size
+    independent flop figure of survey 8(d))."""
+    from paper_2501_02483_b200.ordering import factor_column_counts
+    c = factor_column_counts(pat.pm_pattern).astype(np.float64)
+    return float(np.sum(c * c))
 
 
 def main():

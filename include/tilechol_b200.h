@@ -59,6 +59,11 @@ int tc_etree_fill_count(int64_t n, const int64_t* row_ptr, const int64_t* row_co
 int tc_symbolic_fill_count(int64_t n, const int64_t* col_ptr, const int32_t* row_idx,
                            const int64_t* forward, int64_t* out_nnz_factor);
 
+/* Column counts of L (incl. diagonal) of P A P^T, counts[n]; sum c_j^2 is the
+ * tile-size independent "useful" flop count of survey 8(d). */
+int tc_factor_column_counts(int64_t n, const int64_t* col_ptr, const int32_t* row_idx,
+                            const int64_t* forward, int64_t* counts);
+
 /* reference matcore.py:320-348 structure_stats (bandwidth, thickness). */
 int tc_structure_stats(int64_t n, const int64_t* col_ptr, const int32_t* row_idx,
                        double dense_row_threshold, int64_t* out_bandwidth,

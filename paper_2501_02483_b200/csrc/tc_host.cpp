@@ -367,6 +367,41 @@ extern "C" int tc_symbolic_fill_count(int64_t n, const int64_t* cp, const int32_
     GUARD_END
 }
 
+extern "C" int tc_factor_column_counts(int64_t n, const int64_t* cp, const int32_t* ri, const int64_t* fwd,
+                                       int64_t* counts) {
+    // column counts of L (incl. diagonal) of P A P^T: every (i, r) visited by
+    // the row-subtree walk of etree_count is a nonzero L(i, r)
+    if (n < 1 || !cp || !ri || !counts) return herr(TC_ERR_ARG, "factor_column_counts: bad arguments");
+    GUARD_BEGIN
+    std::vector<int64_t> rp, rc;
+    lower_rows(n, cp, ri, fwd, rp, rc);
+    std::vector<int64_t> par(n, -1), anc(n, -1), mark(n, -1);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            int64_t r = rc[p];
+            while (anc[r] != -1 && anc[r] != i) {
+                const int64_t nx = anc[r];
+                anc[r] = i;
+                r = nx;
+            }
+            if (anc[r] == -1) {
+                anc[r] = i;
+                par[r] = i;
+            }
+        }
+    for (int64_t j = 0; j < n; ++j) counts[j] = 1;
+    for (int64_t i = 0; i < n; ++i) {
+        mark[i] = i;
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+            for (int64_t r = rc[p]; mark[r] != i; r = par[r]) {
+                mark[r] = i;
+                counts[r]++;
+            }
+    }
+    return TC_OK;
+    GUARD_END
+}
+
 extern "C" int tc_structure_stats(int64_t n, const int64_t* cp, const int32_t* ri, double thr, int64_t* bw,
                                   int64_t* th) {
     if (n < 1 || !cp || !ri || !bw || !th) return herr(TC_ERR_ARG, "structure_stats: bad arguments");

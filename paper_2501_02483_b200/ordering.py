@@ -149,6 +149,16 @@ def symbolic_fill_count(m: SymmetricCsc, p: Permutation | None = None) -> FillRe
     return FillReport(nnz_original=m.nnz, nnz_factor=int(out[0]))
 
 
+def factor_column_counts(m: SymmetricCsc, p: Permutation | None = None) -> np.ndarray:
+    """nnz per column of L (incl. diagonal) of P A P^T (C++, etree row subtrees)."""
+    cp, ri = _csc(m)
+    out = np.empty(m.n, dtype=np.int64)
+    f = None if p is None else i64arr(p.forward)
+    check("tc_factor_column_counts", lib.tc_factor_column_counts(
+        m.n, ptr(cp, i64p), ptr(ri, i32p), ptr(f, i64p), ptr(out, i64p)))
+    return out
+
+
 def select_ordering(m: SymmetricCsc, candidates: list[Permutation]) -> Permutation:
     """Identity unless a candidate has a strictly smaller factor; earlier
     candidates win ties (reference ordering.py:266-275)."""

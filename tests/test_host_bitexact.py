@@ -142,3 +142,21 @@ def test_from_coordinates_semantics():
         matcore.from_coordinates(2, [0], [0], [1.0])
     with pytest.raises(MatrixFormatError, match="non-positive"):
         matcore.from_coordinates(2, [0, 1], [0, 1], [1.0, -1.0])
+
+
+@pytest.mark.parametrize("name", CASE_NAMES)
+def test_factor_column_counts_sum_to_fill(name):
+    z = load_case(name)
+    m = _m(z)
+    for f, want in ((None, z["fill"][0]), (z["rcm"], z["fill"][1]), (z["nd"], z["fill"][2])):
+        p = None if f is None else ordering.Permutation.from_forward(f)
+        c = ordering.factor_column_counts(m, p)
+        assert int(c.sum()) == int(want) and c.min() >= 1
+    # against explicit dense symbolic elimination for the small cases
+    if int(z["n"]) <= 200:
+        n = int(z["n"])
+        S = O.dense_of(n, z["cp"], z["ri"], np.ones_like(z["vals"])) != 0
+        for k in range(n):
+            below = k + 1 + np.flatnonzero(S[k + 1:, k])
+            S[np.ix_(below, below)] = True
+        assert np.array_equal(ordering.factor_column_counts(m), np.tril(S).sum(axis=0))
