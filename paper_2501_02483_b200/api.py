@@ -64,7 +64,9 @@ class FactorOptions:
 
     def plan_options(self) -> PlanOptions:
         W = self.workers if self.workers >= 2 else 8
-        thr = -1 if self.tree_reduction == "off" else 0
+        # off: never split; on: the reference rule accum >= 2W;
+        # auto: device default (accum >= 8W, only the genuinely long chains)
+        thr = {"off": -1, "on": 2 * min(W, 16), "auto": 0}[self.tree_reduction]
         return PlanOptions(tree_workers=min(W, 16), tree_threshold=thr, chunk=self.chunk,
                            lookahead=self.lookahead, executor=self.executor)
 

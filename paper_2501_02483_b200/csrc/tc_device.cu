@@ -1213,7 +1213,11 @@ extern "C" int tc_plan_create(int64_t n, int32_t nt, int64_t S, const int32_t* f
     P->W = P->opts.tree_workers > 0 ? P->opts.tree_workers : 8;
     P->fuse = P->opts.reserved[0] == 0;  // reserved[0] = 1 disables POTRF->TRSM streaming
     if (P->W > kMaxW) return set_err(TC_ERR_ARG, "plan_create: tree_workers <= %d", kMaxW);
-    if (P->opts.tree_threshold == 0) P->opts.tree_threshold = 2 * P->W;
+    // The reference rule (chain >= 2 * workers) is sized for CPU threads; on
+    // the device a chain only needs splitting when it is much longer than a
+    // column step's K (the arrow x arrow chains of length ~T), so the default
+    // threshold is 8 * W; 2 * W is available explicitly.
+    if (P->opts.tree_threshold == 0) P->opts.tree_threshold = 8 * P->W;
     P->frow.assign(f_rows, f_rows + S);
     P->fcol.assign(f_cols, f_cols + S);
     P->upd = pick_upd(nt);

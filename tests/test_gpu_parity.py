@@ -205,7 +205,8 @@ def test_factorize_plan_path(torch, name):
 
 @pytest.mark.parametrize("variant", [
     dict(tree_reduction="off"), dict(lookahead=False), dict(executor="direct"), dict(executor="graph"),
-    dict(workers=2), dict(workers=4, chunk=3), dict(workers=16, chunk=1)])
+    dict(workers=2, tree_reduction="on"), dict(workers=4, chunk=3, tree_reduction="on"),
+    dict(workers=16, chunk=1, tree_reduction="on"), dict(workers=2, tree_reduction="on", executor="graph")])
 def test_factorize_plan_variants(torch, variant):
     api, ctsf, matcore, symbolic, impl = _imports()
     for name in ("d1000", "f48", "c500bd"):
