@@ -64,6 +64,7 @@ UpdKernel mk_upd() {
 // no MMA work is wasted on padding (120 -> 40x40, 160/320 -> 80x40,
 // 240/480 -> 80x48), small / odd sizes fall back to predicated 32x32.
 UpdKernel pick_upd(int nt) {
+    if (nt % 64 == 0) return mk_upd<64, 64, 2, 2, 1>();
     if (nt % 80 == 0 && nt % 48 == 0) return mk_upd<80, 48, 2, 2, 1>();
     if (nt % 80 == 0) return mk_upd<80, 40, 2, 1, 2>();
     if (nt % 40 == 0) return mk_upd<40, 40, 1, 1, 4>();
@@ -83,6 +84,7 @@ PersistKernel mk_persist() {
 
 // same block shapes as pick_upd, 256-thread variants (KSPLIT doubled)
 PersistKernel pick_persist(int nt) {
+    if (nt % 64 == 0) return mk_persist<64, 64, 2, 2, 2>();
     if (nt % 80 == 0 && nt % 48 == 0) return mk_persist<80, 48, 2, 2, 2>();
     if (nt % 80 == 0) return mk_persist<80, 40, 2, 1, 4>();
     if (nt % 40 == 0) return mk_persist<40, 40, 1, 1, 8>();
@@ -97,19 +99,22 @@ int prep_kernel(const void* fn, int smem) {
     return TC_OK;
 }
 
+// packed lower block rows in shared memory up to ntp = 184, else in place
 size_t potrf_smem(int nt, bool* in_smem) {
     const int ntp = (nt + 7) & ~7;
-    if (ntp <= 160) {
+    const size_t packed = potrf_packed_doubles(ntp) * 8 + (size_t)ntp * 8;
+    if (packed <= 218 * 1024) {
         *in_smem = true;
-        return (size_t)ntp * pad_ld(ntp) * 8 + (size_t)ntp * 8;
+        return packed;
     }
     *in_smem = false;
     return (size_t)ntp * 8;
 }
 
 bool potrf_supported(int nt) {
-    const int ntp = (nt + 7) & ~7;
-    return ntp <= 160 || nt % 8 == 0;
+    bool in_smem;
+    potrf_smem(nt, &in_smem);
+    return in_smem || nt % 8 == 0;
 }
 
 constexpr int kMaxTrsmNt = 480;
@@ -532,6 +537,7 @@ struct tc_plan {
     int32_t* d_succ = nullptr;
     size_t persist_smem = 0;
     bool fuse = true;  // persistent executor: TRSM(k) streams POTRF(k)'s panels
+    int persist_trsm_ring = 0;  // 0 = auto staging, >0 = strip ring of that many buffers
     int persist_grid = 0;
 };
 
@@ -975,8 +981,24 @@ int build_persistent(tc_plan& P) {
     if (r) return r;
     const PersistKernel K = pick_persist(nt);
     bool in_smem;
-    P.persist_smem = std::max<size_t>({(size_t)K.smem, potrf_smem(nt, &in_smem), trsm_smem_bytes<kPersistTrsmRows>(nt),
-                                       (size_t)4096});
+    // shared memory: the max over task kinds; the fused TRSM may stage L
+    // strip by strip (ring) instead of whole when that lets two CTAs share an SM
+    const size_t base = std::max<size_t>({(size_t)K.smem, potrf_smem(nt, &in_smem), (size_t)4096});
+    const size_t t_full = trsm_smem_bytes<kPersistTrsmRows>(nt);
+    const size_t two_per_sm = 108 * 1024;  // (228 KB - reserved - static) / 2
+    P.persist_trsm_ring = 0;
+    P.persist_smem = std::max(base, t_full);
+    if (P.persist_smem > two_per_sm) {
+        // fused TRSM stages one strip at a time (1 buffer); unfused needs a ring
+        for (int nb : {P.fuse ? 1 : 3, P.fuse ? 1 : 2}) {
+            const size_t t = std::max(base, trsm_smem_ring<kPersistTrsmRows>(nt, nb));
+            if (t <= two_per_sm) {
+                P.persist_trsm_ring = nb < 2 ? 2 : nb;
+                P.persist_smem = t;
+                break;
+            }
+        }
+    }
     r = prep_kernel((const void*)K.fn, (int)P.persist_smem);
     if (r) return r;
     int per_sm = 0, sms = 0;
@@ -1016,6 +1038,7 @@ int run_persistent(tc_plan& P, Lane& ln, cudaStream_t s) {
     potrf_smem(P.nt, &in_smem);
     a.potrf_in_smem = in_smem;
     a.prog = P.fuse ? ln.d_prog : nullptr;
+    a.trsm_ring = P.persist_trsm_ring;
     const PersistKernel K = pick_persist(P.nt);
     K.fn<<<P.persist_grid, kPersistThreads, P.persist_smem, s>>>(a);
     CK(cudaGetLastError());
