@@ -165,7 +165,7 @@ typedef struct tc_plan_opts {
     int32_t tree_workers;   /* W partial accumulators per long chain; 0 = 8 */
     int32_t tree_threshold; /* chains with accum >= threshold are split; 0 = 2*W, <0 = off */
     int32_t chunk;          /* columns per split-K chunk launch; 0 = auto */
-    int32_t lookahead;      /* 1 = split the last contribution off (default); 0 = off */
+    int32_t lookahead;      /* D >= 1: last D contributing columns split off the bulk update; 0 = off */
     int32_t use_graph;      /* 1 = CUDA graph (default), 0 = direct stream launches */
     int32_t reserved[3];
 } tc_plan_opts;

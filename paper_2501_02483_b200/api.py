@@ -46,9 +46,10 @@ class FactorOptions:
     workers: int = 1
     ordering: str = "auto"
     tree_reduction: str = "auto"
-    lookahead: bool = True
+    lookahead: int = 2             # bulk-update lookahead depth in columns (0/False = off)
     executor: str = "persistent"  # persistent | graph | direct
     chunk: int = 0
+    occupancy: int = 0             # persistent CTAs per SM (0 auto, 1, 2)
 
     def __post_init__(self):
         if self.tile_size < 1:
@@ -68,7 +69,8 @@ class FactorOptions:
         # auto: device default (accum >= 8W, only the genuinely long chains)
         thr = {"off": -1, "on": 2 * min(W, 16), "auto": 0}[self.tree_reduction]
         return PlanOptions(tree_workers=min(W, 16), tree_threshold=thr, chunk=self.chunk,
-                           lookahead=self.lookahead, executor=self.executor)
+                           lookahead=self.lookahead, executor=self.executor,
+                           occupancy=self.occupancy)
 
 
 @dataclass(eq=False)

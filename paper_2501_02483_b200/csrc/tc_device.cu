@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -64,6 +65,11 @@ UpdKernel mk_upd() {
 // no MMA work is wasted on padding (120 -> 40x40, 160/320 -> 80x40,
 // 240/480 -> 80x48), small / odd sizes fall back to predicated 32x32.
 UpdKernel pick_upd(int nt) {
+    if (const char* f = getenv("TC_PERSIST_SHAPE")) {  // tuning override (kept in step with pick_persist)
+        if (!strcmp(f, "64")) return mk_upd<64, 64, 2, 2, 1>();
+        if (!strcmp(f, "32")) return mk_upd<32, 32, 2, 2, 1>();
+        if (!strcmp(f, "40")) return mk_upd<40, 40, 1, 1, 4>();
+    }
     if (nt % 64 == 0) return mk_upd<64, 64, 2, 2, 1>();
     if (nt % 80 == 0 && nt % 48 == 0) return mk_upd<80, 48, 2, 2, 1>();
     if (nt % 80 == 0) return mk_upd<80, 40, 2, 1, 2>();
@@ -78,18 +84,25 @@ struct PersistKernel {
 };
 
 template <int BM, int BN, int WGM, int WGN, int KS>
-PersistKernel mk_persist() {
-    return PersistKernel{k_persist<BM, BN, WGM, WGN, KS>, BM, BN, UpdCfg<BM, BN, WGM, WGN, KS>::SMEM};
+PersistKernel mk_persist(int minb) {
+    return PersistKernel{minb == 2 ? k_persist<BM, BN, WGM, WGN, KS, 2> : k_persist<BM, BN, WGM, WGN, KS, 1>, BM, BN,
+                         UpdCfg<BM, BN, WGM, WGN, KS>::SMEM};
 }
 
-// same block shapes as pick_upd, 256-thread variants (KSPLIT doubled)
-PersistKernel pick_persist(int nt) {
-    if (nt % 64 == 0) return mk_persist<64, 64, 2, 2, 2>();
-    if (nt % 80 == 0 && nt % 48 == 0) return mk_persist<80, 48, 2, 2, 2>();
-    if (nt % 80 == 0) return mk_persist<80, 40, 2, 1, 4>();
-    if (nt % 40 == 0) return mk_persist<40, 40, 1, 1, 8>();
-    if (nt >= 96) return mk_persist<64, 64, 2, 2, 2>();
-    return mk_persist<32, 32, 2, 2, 2>();
+// same block shapes as pick_upd, 256-thread variants (KSPLIT doubled);
+// minb = minimum resident CTAs per SM the variant is compiled for
+PersistKernel pick_persist(int nt, int minb) {
+    if (const char* f = getenv("TC_PERSIST_SHAPE")) {  // tuning override
+        if (!strcmp(f, "64")) return mk_persist<64, 64, 2, 2, 2>(minb);
+        if (!strcmp(f, "32")) return mk_persist<32, 32, 2, 2, 2>(minb);
+        if (!strcmp(f, "40")) return mk_persist<40, 40, 1, 1, 8>(minb);
+    }
+    if (nt % 64 == 0) return mk_persist<64, 64, 2, 2, 2>(minb);
+    if (nt % 80 == 0 && nt % 48 == 0) return mk_persist<80, 48, 2, 2, 2>(minb);
+    if (nt % 80 == 0) return mk_persist<80, 40, 2, 1, 4>(minb);
+    if (nt % 40 == 0) return mk_persist<40, 40, 1, 1, 8>(minb);
+    if (nt >= 96) return mk_persist<64, 64, 2, 2, 2>(minb);
+    return mk_persist<32, 32, 2, 2, 2>(minb);
 }
 
 int prep_kernel(const void* fn, int smem) {
@@ -524,7 +537,7 @@ struct tc_plan {
     int prio_hi = 0, prio_lo = 0;
     int dev = 0;
     // per-column launch ids (persistent ticket order)
-    std::vector<int32_t> colB, colL, colPot, colTrsm;
+    std::vector<int32_t> colB, colM, colL, colPot, colTrsm;
     std::vector<std::vector<int32_t>> colComb, colChunk;
     // persistent executor
     std::vector<PTask> ptasks;
@@ -538,6 +551,7 @@ struct tc_plan {
     size_t persist_smem = 0;
     bool fuse = true;  // persistent executor: TRSM(k) streams POTRF(k)'s panels
     int persist_trsm_ring = 0;  // 0 = auto staging, >0 = strip ring of that many buffers
+    int persist_minb = 2;
     int persist_grid = 0;
 };
 
@@ -646,6 +660,7 @@ int build_plan(tc_plan& P) {
     // ---- pass 2: launches in topological order
     P.launches.clear();
     P.colB.assign(T, -1);
+    P.colM.assign(T, -1);
     P.colL.assign(T, -1);
     P.colPot.assign(T, -1);
     P.colTrsm.assign(T, -1);
@@ -675,9 +690,22 @@ int build_plan(tc_plan& P) {
 
     for (int k = 0; k < T; ++k) {
         const int64_t c0 = P.cs[k], c1 = P.cs[k + 1];
-        const int32_t nlast = (P.opts.lookahead && rp[k + 1] > rp[k]) ? rn[rp[k + 1] - 1] : -1;
+        // lookahead depth D: the last contributing column feeds L(k), the
+        // D-1 before it feed M(k), the rest feed the bulk update B(k), so
+        // B(k+D) can run while columns k-1 .. k+D-1 are still in flight
+        const int D = P.opts.lookahead;
+        const int64_t nctr = rp[k + 1] - rp[k];
+        const int32_t nlast = (D > 0 && nctr > 0) ? rn[rp[k + 1] - 1] : -1;
+        const int32_t nmid = (D > 1 && nctr > 1) ? rn[std::max<int64_t>(rp[k], rp[k + 1] - D)] : -1;
+        const int32_t bcut = nmid >= 0 ? nmid : (nlast >= 0 ? nlast : INT32_MAX);
+        // first pair of target t whose contributing column is >= col
+        auto cut = [&](int64_t t, int32_t col) {
+            int64_t x = tp1[t];
+            while (x > tp0[t] && P.fcol[P.pairs[x - 1].b] >= col) --x;
+            return x;
+        };
         // B(k): bulk pairs of non-reduced targets
-        int32_t bnode = -1, lnode = -1;
+        int32_t bnode = -1, lnode = -1, mnode = -1;
         {
             Launch L;
             L.kind = L_UPD;
@@ -685,8 +713,7 @@ int build_plan(tc_plan& P) {
             std::vector<int32_t> cols;
             for (int64_t t = c0; t < c1; ++t) {
                 if (red_base[t] >= 0) continue;
-                int64_t p1 = tp1[t];
-                if (nlast >= 0 && p1 > tp0[t] && P.fcol[P.pairs[p1 - 1].b] == nlast) --p1;
+                const int64_t p1 = cut(t, bcut);
                 if (p1 > tp0[t]) {
                     emit_items(t, tp0[t], p1, (int32_t)t, MODE_SUB);
                     for (int64_t x = tp0[t]; x < p1; ++x) cols.push_back(P.fcol[P.pairs[x].b]);
@@ -701,6 +728,30 @@ int build_plan(tc_plan& P) {
                 P.launches.push_back(std::move(L));
             }
         }
+        if (nmid >= 0) {
+            Launch L;
+            L.kind = L_UPD;
+            L.off = (int64_t)P.items.size();
+            std::vector<int32_t> cols;
+            for (int64_t t = c0; t < c1; ++t) {
+                if (red_base[t] >= 0) continue;
+                const int64_t p0 = cut(t, nmid), p1 = cut(t, nlast);
+                if (p1 > p0) {
+                    emit_items(t, p0, p1, (int32_t)t, MODE_SUB);
+                    for (int64_t x = p0; x < p1; ++x) cols.push_back(P.fcol[P.pairs[x].b]);
+                    L.flops += (P.frow[t] == k ? 1.0 : 2.0) * n3 * (double)(p1 - p0);
+                }
+            }
+            L.cnt = (int64_t)P.items.size() - L.off;
+            if (L.cnt > 0) {
+                add_panel_deps(L.deps, cols);
+                if (bnode >= 0) L.deps.push_back(bnode);
+                mnode = (int32_t)P.launches.size();
+                P.colM[k] = mnode;
+                P.launches.push_back(std::move(L));
+            }
+        }
+        const int32_t prev = mnode >= 0 ? mnode : bnode;  // last writer of column k before L(k)
         if (nlast >= 0) {
             Launch L;
             L.kind = L_UPD;
@@ -718,7 +769,7 @@ int build_plan(tc_plan& P) {
             L.cnt = (int64_t)P.items.size() - L.off;
             if (L.cnt > 0) {
                 L.deps.push_back(pnode[nlast]);
-                if (bnode >= 0) L.deps.push_back(bnode);
+                if (prev >= 0) L.deps.push_back(prev);
                 lnode = (int32_t)P.launches.size();
                 P.colL[k] = lnode;
                 P.launches.push_back(std::move(L));
@@ -752,6 +803,7 @@ int build_plan(tc_plan& P) {
             L.k = k;
             L.slot = c0;
             if (bnode >= 0) L.deps.push_back(bnode);
+            if (mnode >= 0) L.deps.push_back(mnode);
             if (lnode >= 0) L.deps.push_back(lnode);
             for (int32_t x : comb_diag) L.deps.push_back(x);
             L.flops += n3 / 3.0;
@@ -772,6 +824,7 @@ int build_plan(tc_plan& P) {
             L.cnt = c1 - c0 - 1;
             L.deps.push_back(pot);
             if (bnode >= 0) L.deps.push_back(bnode);
+            if (mnode >= 0) L.deps.push_back(mnode);
             if (lnode >= 0) L.deps.push_back(lnode);
             for (int32_t x : comb_off) L.deps.push_back(x);
             L.flops += n3 * (double)(c1 - c0 - 1);
@@ -889,13 +942,17 @@ int build_persistent(tc_plan& P) {
         std::sort(pdeps[i].begin(), pdeps[i].end());
         pdeps[i].erase(std::unique(pdeps[i].begin(), pdeps[i].end()), pdeps[i].end());
     }
-    if (T > 0) put(P.colB[0]);
+    const int D = std::max(1, P.opts.lookahead);
+    for (int j = 0; j < std::min(D, T); ++j) put(P.colB[j]);
     for (int k = 0; k < T; ++k) {
+        put(P.colM[k]);
         put(P.colL[k]);
         for (int32_t c : P.colComb[k]) put(c);
         put(P.colPot[k]);
         if (fuse) put(P.colTrsm[k]);
+        if (k + D < T) put(P.colB[k + D]);
         if (k + 1 < T) put(P.colB[k + 1]);
+        if (k + 1 < T) put(P.colM[k + 1]);
         put(P.colTrsm[k]);
         for (int32_t c : P.colChunk[k]) put(c);
     }
@@ -979,7 +1036,11 @@ int build_persistent(tc_plan& P) {
     if (!r) r = upload(P.p_succ_ptr, &P.d_succ_ptr, s0);
     if (!r) r = upload(P.p_succ, &P.d_succ, s0);
     if (r) return r;
-    const PersistKernel K = pick_persist(nt);
+    // occupancy mode (opts.reserved[1]): 1 = one CTA/SM (no register cap,
+    // whole-L TRSM staging), 2 = two CTAs/SM when the smem plan fits, 0 = auto
+    const int occ_mode = P.opts.reserved[1];
+    P.persist_minb = occ_mode == 1 ? 1 : 2;
+    const PersistKernel K = pick_persist(nt, P.persist_minb);
     bool in_smem;
     // shared memory: the max over task kinds; the fused TRSM may stage L
     // strip by strip (ring) instead of whole when that lets two CTAs share an SM
@@ -988,7 +1049,7 @@ int build_persistent(tc_plan& P) {
     const size_t two_per_sm = 108 * 1024;  // (228 KB - reserved - static) / 2
     P.persist_trsm_ring = 0;
     P.persist_smem = std::max(base, t_full);
-    if (P.persist_smem > two_per_sm) {
+    if (P.persist_minb == 2 && P.persist_smem > two_per_sm) {
         // fused TRSM stages one strip at a time (1 buffer); unfused needs a ring
         for (int nb : {P.fuse ? 1 : 3, P.fuse ? 1 : 2}) {
             const size_t t = std::max(base, trsm_smem_ring<kPersistTrsmRows>(nt, nb));
@@ -1039,7 +1100,7 @@ int run_persistent(tc_plan& P, Lane& ln, cudaStream_t s) {
     a.potrf_in_smem = in_smem;
     a.prog = P.fuse ? ln.d_prog : nullptr;
     a.trsm_ring = P.persist_trsm_ring;
-    const PersistKernel K = pick_persist(P.nt);
+    const PersistKernel K = pick_persist(P.nt, P.persist_minb);
     K.fn<<<P.persist_grid, kPersistThreads, P.persist_smem, s>>>(a);
     CK(cudaGetLastError());
     return TC_OK;

@@ -37,8 +37,10 @@ class PlanOptions:
     tree_workers: int = 8        # W partial accumulators per long chain
     tree_threshold: int = 0      # 0 = 2*W (reference rule), < 0 = no tree reduction
     chunk: int = 0               # columns per split-K launch (0 = 8)
-    lookahead: bool = True
+    lookahead: int = 2           # columns of lookahead for the bulk update (0 = off)
     executor: str = "persistent"  # persistent | graph | direct
+    occupancy: int = 0            # persistent CTAs per SM: 0 auto (2 when it fits), 1, 2
+    fuse_trsm: bool = True        # persistent: TRSM(k) streams POTRF(k)'s panels
 
     def to_c(self) -> PlanOpts:
         o = PlanOpts()
@@ -47,6 +49,8 @@ class PlanOptions:
         o.chunk = self.chunk
         o.lookahead = int(self.lookahead)
         o.use_graph = {"direct": 0, "graph": 1, "persistent": 2}[self.executor]
+        o.reserved[0] = 0 if self.fuse_trsm else 1
+        o.reserved[1] = int(self.occupancy)
         return o
 
 

@@ -204,7 +204,7 @@ def test_factorize_plan_path(torch, name):
 
 
 @pytest.mark.parametrize("variant", [
-    dict(tree_reduction="off"), dict(lookahead=False), dict(executor="direct"), dict(executor="graph"),
+    dict(tree_reduction="off"), dict(lookahead=False), dict(lookahead=3), dict(lookahead=3, executor="graph"), dict(executor="direct"), dict(executor="graph"),
     dict(workers=2, tree_reduction="on"), dict(workers=4, chunk=3, tree_reduction="on"),
     dict(workers=16, chunk=1, tree_reduction="on"), dict(workers=2, tree_reduction="on", executor="graph")])
 def test_factorize_plan_variants(torch, variant):

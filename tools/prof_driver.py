@@ -15,9 +15,10 @@ ap.add_argument("--workload", default="c2")
 ap.add_argument("--tile", type=int, default=120)
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--executor", default="persistent")
+ap.add_argument("--ordering", default="auto")
 a = ap.parse_args()
 m = bench.build_matrix(a.workload)
-opts = api.FactorOptions(tile_size=a.tile, executor=a.executor)
+opts = api.FactorOptions(tile_size=a.tile, executor=a.executor, ordering=a.ordering)
 pat = api._pattern_for(m, opts)
 plan = pat.plan
 vals = torch.from_numpy(np.ascontiguousarray(pat.permuted_values(m))).cuda()
