@@ -206,6 +206,13 @@ void tc_plan_destroy(tc_plan_t p);
  * count and algorithmic flops.  Factorises storage_dev in place. */
 int tc_plan_profile(tc_plan_t p, double* storage_dev, void* stream, int32_t n_cls, double* ms,
                     int64_t* counts, double* flops);
+/* Persistent-executor task trace (diagnostics): factorises storage_dev once
+ * and returns per task [ticket_ns, start_ns, end_ns, sm_id] (tasks_out[cap][4])
+ * and its launch id, per launch [kind, column, class] (launch_meta[NL][3]).
+ * With cap < n_tasks or launch_cap < n_launches only the sizes are returned. */
+int tc_plan_trace(tc_plan_t p, double* storage_dev, void* stream, int64_t cap, int64_t* tasks_out,
+                  int32_t* task_launch, int64_t launch_cap, int32_t* launch_meta, int64_t* n_tasks,
+                  int64_t* n_launches);
 /* FP64 tensor-pipe (DMMA m8n8k4) throughput microbenchmark, TFLOP/s. */
 int tc_bench_dmma_peak(int64_t iters, int32_t blocks_per_sm, int32_t warps_per_block,
                        double* tflops);

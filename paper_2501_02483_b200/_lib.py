@@ -85,6 +85,7 @@ SIGNATURES = {
     "tc_plan_pack": (C.c_int, [vp, vp, vp, i64, vp, vp]),
     "tc_plan_destroy": (None, [vp]),
     "tc_plan_profile": (C.c_int, [vp, vp, vp, i32, f64p, i64p, f64p]),
+    "tc_plan_trace": (C.c_int, [vp, vp, vp, i64, i64p, i32p, i64, i32p, i64p, i64p]),
     "tc_bench_dmma_peak": (C.c_int, [i64, i32, i32, f64p]),
 }
 

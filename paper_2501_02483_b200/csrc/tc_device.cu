@@ -503,6 +503,7 @@ struct Lane {
     cudaGraph_t graph = nullptr;
     int32_t* d_pstate = nullptr;  // persistent: [remaining | deps_left | ticket]
     int32_t* d_prog = nullptr;    // persistent fused: per-column POTRF panel progress [T]
+    int64_t* d_trace = nullptr;   // persistent: per-task timestamps (tc_plan_trace only)
     Ctx h{};
 };
 
@@ -709,6 +710,7 @@ int build_plan(tc_plan& P) {
         {
             Launch L;
             L.kind = L_UPD;
+            L.k = k;
             L.off = (int64_t)P.items.size();
             std::vector<int32_t> cols;
             for (int64_t t = c0; t < c1; ++t) {
@@ -731,6 +733,7 @@ int build_plan(tc_plan& P) {
         if (nmid >= 0) {
             Launch L;
             L.kind = L_UPD;
+            L.k = k;
             L.off = (int64_t)P.items.size();
             std::vector<int32_t> cols;
             for (int64_t t = c0; t < c1; ++t) {
@@ -755,6 +758,7 @@ int build_plan(tc_plan& P) {
         if (nlast >= 0) {
             Launch L;
             L.kind = L_UPD;
+            L.k = k;
             L.high = 1;
             L.cls = 1;
             L.off = (int64_t)P.items.size();
@@ -841,6 +845,7 @@ int build_plan(tc_plan& P) {
             const int w = pcs[u].j % W;
             Launch L;
             L.kind = L_UPD;
+            L.k = k;
             L.cls = 6;
             L.off = (int64_t)P.items.size();
             std::vector<int32_t> cols;
@@ -1100,6 +1105,7 @@ int run_persistent(tc_plan& P, Lane& ln, cudaStream_t s) {
     a.potrf_in_smem = in_smem;
     a.prog = P.fuse ? ln.d_prog : nullptr;
     a.trsm_ring = P.persist_trsm_ring;
+    a.trace = ln.d_trace;
     const PersistKernel K = pick_persist(P.nt, P.persist_minb);
     K.fn<<<P.persist_grid, kPersistThreads, P.persist_smem, s>>>(a);
     CK(cudaGetLastError());
@@ -1542,6 +1548,41 @@ extern "C" int tc_plan_profile(tc_plan_t p, double* storage, void* stream, int32
         flops[c] += p->launches[i].flops;
     }
     for (auto& e : ev) cudaEventDestroy(e);
+    return TC_OK;
+}
+
+// Task trace of one persistent-executor factorisation: per task (ticket
+// order) the ns timestamps when its CTA took the ticket, when the task's
+// launch became runnable and when the task finished, and the SM id; per
+// launch its kind (0 update, 1 POTRF, 2 TRSM, 3 combine, 4 logdet), column
+// and profiling class.  Factorises storage_dev in place.
+extern "C" int tc_plan_trace(tc_plan_t p, double* storage, void* stream, int64_t cap, int64_t* tasks_out,
+                             int32_t* task_launch, int64_t launch_cap, int32_t* launch_meta, int64_t* n_tasks,
+                             int64_t* n_launches) {
+    if (!p || !storage || !n_tasks || !n_launches) return set_err(TC_ERR_ARG, "plan_trace: bad arguments");
+    if (p->opts.use_graph != 2) return set_err(TC_ERR_ARG, "plan_trace: persistent executor only");
+    const int64_t NT = (int64_t)p->ptasks.size(), NL = (int64_t)p->launches.size();
+    *n_tasks = NT;
+    *n_launches = NL;
+    if (cap < NT || launch_cap < NL || !tasks_out || !task_launch || !launch_meta) return TC_OK;  // size query
+    int r = ensure_lane(*p, 0);
+    if (r) return r;
+    Lane& ln = p->lanes[0];
+    cudaStream_t s = (cudaStream_t)stream;
+    CK(cudaMalloc(&ln.d_trace, (size_t)NT * 4 * sizeof(int64_t)));
+    CK(cudaMemsetAsync(ln.d_trace, 0, (size_t)NT * 4 * sizeof(int64_t), s));
+    r = tc_plan_factorize_async(p, 0, storage, stream);
+    if (!r) CK(cudaMemcpyAsync(tasks_out, ln.d_trace, (size_t)NT * 4 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    cudaFree(ln.d_trace);
+    ln.d_trace = nullptr;
+    if (r) return r;
+    for (int64_t t = 0; t < NT; ++t) task_launch[t] = p->ptasks[t].launch;
+    for (int64_t i = 0; i < NL; ++i) {
+        launch_meta[3 * i] = p->launches[i].kind;
+        launch_meta[3 * i + 1] = p->launches[i].k;
+        launch_meta[3 * i + 2] = p->launches[i].cls;
+    }
     return TC_OK;
 }
 
