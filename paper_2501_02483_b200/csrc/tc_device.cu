@@ -504,6 +504,7 @@ struct Lane {
     int32_t* d_pstate = nullptr;  // persistent: [remaining | deps_left | ticket]
     int32_t* d_prog = nullptr;    // persistent fused: per-column POTRF panel progress [T]
     int64_t* d_trace = nullptr;   // persistent: per-task timestamps (tc_plan_trace only)
+    int32_t* d_xctr = nullptr;    // persistent: fused diagonal SYRK TRSM warp panel flags [T][32]
     Ctx h{};
 };
 
@@ -554,6 +555,11 @@ struct tc_plan {
     int persist_trsm_ring = 0;  // 0 = auto staging, >0 = strip ring of that many buffers
     int persist_minb = 2;
     int persist_grid = 0;
+    // fused diagonal SYRK: POTRF(k) applies the last update of its diagonal
+    // tile itself, consuming L(k, n_last) panel by panel from TRSM(n_last)
+    std::vector<int64_t> xslot_of_col;  // [T] slot of L(k, n_last) or -1
+    int32_t* d_xctr_of_slot = nullptr;  // [S] consuming column or -1
+    int nfused = 0;
 };
 
 namespace {
@@ -947,6 +953,46 @@ int build_persistent(tc_plan& P) {
         std::sort(pdeps[i].begin(), pdeps[i].end());
         pdeps[i].erase(std::unique(pdeps[i].begin(), pdeps[i].end()), pdeps[i].end());
     }
+    // Fused diagonal SYRK (packed in-smem POTRF only): the diagonal tile's
+    // items leave L(k); POTRF(k) no longer waits for L(k) but streams the
+    // published panels of L(k, n_last) (TRSM(n_last) is ticketed earlier).
+    // L(k) keeps the off-diagonal targets (TRSM(k) still depends on it); an
+    // L(k) left empty is dropped from the DAG.
+    std::vector<int64_t> loff(NL), lcnt(NL);
+    for (size_t i = 0; i < NL; ++i) {
+        loff[i] = P.launches[i].off;
+        lcnt[i] = P.launches[i].cnt;
+    }
+    std::vector<char> dead(NL, 0);
+    P.xslot_of_col.assign(T, -1);
+    P.nfused = 0;
+    bool pin_smem;
+    potrf_smem(nt, &pin_smem);
+    // experimental (off by default: the per-panel TRSM publication costs more
+    // than the LAST hand-off it removes); TC_SYRK_FUSE=1 enables
+    const bool fuse_syrk = TC_SYRK_FUSE_CODE && pin_smem && getenv("TC_SYRK_FUSE") != nullptr;
+    for (int k = 0; k < T && fuse_syrk; ++k) {
+        const int32_t lk = P.colL[k];
+        if (lk < 0) continue;
+        int64_t nd = 0;
+        while (nd < lcnt[lk] && P.items[loff[lk] + nd].dst == (int32_t)P.cs[k]) ++nd;
+        if (nd == 0) continue;
+        const Item& it0 = P.items[loff[lk]];
+        if (it0.p1 - it0.p0 != 1) continue;
+        const Pair pr = P.pairs[it0.p0];
+        if (pr.a != pr.b) continue;
+        P.xslot_of_col[k] = pr.a;
+        ++P.nfused;
+        loff[lk] += nd;
+        lcnt[lk] -= nd;
+        if (lcnt[lk] == 0) dead[lk] = 1;
+        auto& pd = pdeps[P.colPot[k]];
+        pd.erase(std::remove(pd.begin(), pd.end(), lk), pd.end());
+    }
+    for (size_t i = 0; i < NL; ++i) {
+        auto& pd = pdeps[i];
+        pd.erase(std::remove_if(pd.begin(), pd.end(), [&](int32_t d) { return dead[d] != 0; }), pd.end());
+    }
     const int D = std::max(1, P.opts.lookahead);
     for (int j = 0; j < std::min(D, T); ++j) put(P.colB[j]);
     for (int k = 0; k < T; ++k) {
@@ -980,9 +1026,14 @@ int build_persistent(tc_plan& P) {
     for (int32_t id : order) {
         const Launch& L = P.launches[id];
         const size_t before = P.ptasks.size();
+        if (dead[id]) {
+            P.p_remaining[id] = 0;
+            P.p_deps[id] = 0;
+            continue;
+        }
         switch (L.kind) {
             case L_UPD:
-                for (int64_t x = L.off; x < L.off + L.cnt; ++x) P.ptasks.push_back(PTask{id, (int32_t)x, 0});
+                for (int64_t x = loff[id]; x < loff[id] + lcnt[id]; ++x) P.ptasks.push_back(PTask{id, (int32_t)x, 0});
                 break;
             case L_TRSM:
                 for (int64_t x = L.off; x < L.off + L.cnt; ++x)
@@ -1017,6 +1068,7 @@ int build_persistent(tc_plan& P) {
                 q.k = L.k;
                 q.slot = L.slot;
                 q.live = (int32_t)std::min<int64_t>(P.n - (int64_t)L.k * nt, nt);
+                q.scratch0 = P.xslot_of_col[L.k];  // fused SYRK source slot or -1
                 break;
             case L_TRSM:
                 q.kind = 2;
@@ -1040,16 +1092,28 @@ int build_persistent(tc_plan& P) {
     if (!r) r = upload(init, &P.d_p_init, s0);
     if (!r) r = upload(P.p_succ_ptr, &P.d_succ_ptr, s0);
     if (!r) r = upload(P.p_succ, &P.d_succ, s0);
+    if (!r) {
+        std::vector<int32_t> xos(P.S, -1);
+        for (int k = 0; k < T; ++k)
+            if (P.xslot_of_col[k] >= 0) xos[P.xslot_of_col[k]] = k;
+        r = upload(xos, &P.d_xctr_of_slot, s0);
+    }
     if (r) return r;
     // occupancy mode (opts.reserved[1]): 1 = one CTA/SM (no register cap,
     // whole-L TRSM staging), 2 = two CTAs/SM when the smem plan fits, 0 = auto
+    // auto: a plan whose column steps carry little update work is bound by
+    // the POTRF -> TRSM -> update chain, which runs ~1.3x faster with the SM
+    // to itself (C2: 0.15 GFLOP per column); update-heavy plans (C3, C4:
+    // 0.7-0.9 GFLOP per column at nt=120) need the second CTA per SM to hide
+    // the update pipeline's bubbles
     const int occ_mode = P.opts.reserved[1];
-    P.persist_minb = occ_mode == 1 ? 1 : 2;
+    P.persist_minb = occ_mode == 1 ? 1 : occ_mode == 2 ? 2 : (P.flops / std::max(1, P.T) < 4.0e8 ? 1 : 2);
     const PersistKernel K = pick_persist(nt, P.persist_minb);
     bool in_smem;
     // shared memory: the max over task kinds; the fused TRSM may stage L
     // strip by strip (ring) instead of whole when that lets two CTAs share an SM
-    const size_t base = std::max<size_t>({(size_t)K.smem, potrf_smem(nt, &in_smem), (size_t)4096});
+    const size_t xs_bytes = P.nfused ? (size_t)8 * pad_ld((nt + 7) & ~7) * sizeof(double) : 0;
+    const size_t base = std::max<size_t>({(size_t)K.smem, potrf_smem(nt, &in_smem) + xs_bytes, (size_t)4096});
     const size_t t_full = trsm_smem_bytes<kPersistTrsmRows>(nt);
     const size_t two_per_sm = 108 * 1024;  // (228 KB - reserved - static) / 2
     P.persist_trsm_ring = 0;
@@ -1085,6 +1149,10 @@ int run_persistent(tc_plan& P, Lane& ln, cudaStream_t s) {
         if (!ln.d_prog) CK(cudaMalloc(&ln.d_prog, (size_t)P.T * sizeof(int32_t)));
         CK(cudaMemsetAsync(ln.d_prog, 0, (size_t)P.T * sizeof(int32_t), s));
     }
+    if (P.nfused) {
+        if (!ln.d_xctr) CK(cudaMalloc(&ln.d_xctr, (size_t)P.T * 32 * sizeof(int32_t)));
+        CK(cudaMemsetAsync(ln.d_xctr, 0, (size_t)P.T * 32 * sizeof(int32_t), s));
+    }
     PersistArgs a{};
     a.ctx = ln.d_ctx;
     a.items = P.d_items;
@@ -1106,6 +1174,9 @@ int run_persistent(tc_plan& P, Lane& ln, cudaStream_t s) {
     a.prog = P.fuse ? ln.d_prog : nullptr;
     a.trsm_ring = P.persist_trsm_ring;
     a.trace = ln.d_trace;
+    a.xctr = P.nfused ? ln.d_xctr : nullptr;
+    a.xctr_of_slot = P.d_xctr_of_slot;
+    a.xper = ((P.nt + kPersistTrsmRows - 1) / kPersistTrsmRows) * (kPersistTrsmRows / 8);
     const PersistKernel K = pick_persist(P.nt, P.persist_minb);
     K.fn<<<P.persist_grid, kPersistThreads, P.persist_smem, s>>>(a);
     CK(cudaGetLastError());
@@ -1478,12 +1549,14 @@ extern "C" void tc_plan_destroy(tc_plan_t p) {
         cudaFree(ln.d_scratch);
         cudaFree(ln.d_pstate);
         cudaFree(ln.d_prog);
+        cudaFree(ln.d_xctr);
     }
     cudaFree(p->d_ptasks);
     cudaFree(p->d_plaunch);
     cudaFree(p->d_p_init);
     cudaFree(p->d_succ_ptr);
     cudaFree(p->d_succ);
+    cudaFree(p->d_xctr_of_slot);
     cudaFree(p->d_items);
     cudaFree(p->d_pairs);
     cudaFree(p->d_tgts);

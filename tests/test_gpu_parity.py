@@ -315,3 +315,41 @@ def test_c1_config_end_to_end(torch):
     x = api.solve(ctx, b)
     xr = O.tile_solve(ref, fsm, m.n, nt, b)
     assert np.linalg.norm(x - xr) / np.linalg.norm(xr) <= SOLVE_TOL
+
+
+def _vs_oracle(m, nt, **opts):
+    """Factor through the public API and check factor / backward error /
+    logdet / solve against the oracle executor on the same inputs."""
+    api, ctsf, matcore, symbolic, impl = _imports()
+    ctx = api.factorize(m, api.FactorOptions(tile_size=nt, **opts))
+    fg = ctx.symbolic.factor_grid
+    fsm = fg.slot_map
+    op, dst, s1, s2, _ = O.compile_ops(O.task_stream(fsm.shape[0], fsm), fsm, fg.n_tiles)
+    assert ctx.permutation.is_identity()
+    pm = m
+    tpl = ctsf.pack_into_grid(pm, fg).storage
+    ref = tpl.copy()
+    p, info = O.run_ops(ref, np.zeros((0, nt, nt)), op, dst, s1, s2, 0, op.size)
+    assert info == -1
+    assert relf(ctx.factor.host_storage(), ref) < FACTOR_TOL
+    e2 = impl.replay_residual(ctx.factor.storage, tpl, op, dst, s1, s2, fg.tile_rows == fg.tile_cols)
+    assert np.sqrt(e2) / anorm_f(pm.col_ptr, pm.values) <= BACKWARD_TOL
+    ld_ref = O.logdet(ref, fsm, pm.n, nt)
+    assert abs(api.logdet(ctx) - ld_ref) <= LOGDET_TOL * abs(ld_ref)
+
+
+@pytest.mark.parametrize("nt", [40, 64, 120])
+@pytest.mark.parametrize("occ", [1, 2])
+def test_inla_small_with_fill(torch, nt, occ):
+    """Small INLA precision (block-tridiagonal + arrow, fill tiles) through the
+    persistent executor, both occupancies (fused diagonal SYRK streaming)."""
+    from paper_2501_02483_b200 import workloads as W
+    m = W.InlaFamily(nx=10, ny=12, nsteps=20, nfix=3).matrix(0.5, 0.9, 1e-3)
+    _vs_oracle(m, nt, ordering="identity", occupancy=occ)
+
+
+@pytest.mark.parametrize("occ", [1, 2])
+def test_variable_band_small(torch, occ):
+    from paper_2501_02483_b200 import workloads as W
+    m = W.c2_variable_band(n=6000, t=40, seg_len=600, max_band=300)
+    _vs_oracle(m, 48, ordering="identity", occupancy=occ)
