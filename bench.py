@@ -34,6 +34,7 @@ WORKLOADS = {
     "c2": ("variable-band arrowhead n=100,000 max band 1,000 t=200 (BASELINE config 2)", 120),
     "c3": ("INLA 2000x100+10 (n=200,010) kappa=.5 rho=.9 tau=1e-3 (BASELINE config 3)", 240),
     "c4": ("arrowhead n=1,000,000 b=2000 t=500 (BASELINE config 4)", 240),
+    "c5": ("batch of 64 INLA factorizations (C3 pattern, theta on a 4x4x4 grid) (BASELINE config 5)", 120),
 }
 PEAKS_FILE = os.path.join(ROOT, "profiles", "fp64_peaks.json")
 FP64_FALLBACK_TFLOPS = 37.0  # NVIDIA B200 FP64 (tensor) nominal, used only if unmeasured
@@ -55,6 +56,7 @@ def parse():
     ap.add_argument("--executor", default="persistent", choices=["persistent", "graph", "direct"])
     ap.add_argument("--lookahead", type=int, default=None, help="bulk-update lookahead depth (default: api default)")
     ap.add_argument("--occupancy", type=int, default=0, help="persistent CTAs/SM: 0 auto, 1, 2")
+    ap.add_argument("--lanes", type=int, default=4, help="c5: factorisations in flight per GPU")
     ap.add_argument("--ordering", default="auto",
                     help="auto (SPEC policy) | identity (C4: auto provably picks identity, zero fill)")
     return ap.parse_args()
@@ -62,6 +64,8 @@ def parse():
 
 def build_matrix(name):
     from paper_2501_02483_b200 import workloads as W
+    if name == "c5":
+        return W.c3()
     if name == "c1":
         return W.c1()
     if name == "c2":
@@ -175,6 +179,18 @@ def fp64_peak():
         return float(d["fp64_peak_tflops"]), "measured (profiles/fp64_peaks.json: max of DMMA microbenchmark and cuBLAS DGEMM)"
     except (OSError, KeyError, ValueError):
         return FP64_FALLBACK_TFLOPS, "fallback nominal B200 FP64 (unmeasured)"
+
+
+def traffic_of(name, nt):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel per
+    launch, from the committed ncu --set full capture (profiles/traffic.json),
+    or None when this workload/tile was not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f).get(f"{name}@{nt}")
+        return (float(d["bytes_per_launch"]), d.get("source", "")) if d else (None, "")
+    except (OSError, ValueError, KeyError):
+        return None, ""
 
 
 def hbm_peak():
@@ -294,8 +310,133 @@ def run_reference(a, name, nt, desc):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------- GPU arm, batch --
+def run_batch(a, nt, desc, rank, world):
+    """C5: 64 INLA factorisations Q(theta) sharing the C3 pattern, sharded in
+    contiguous blocks over the ranks (strong scaling), `lanes` in flight per
+    GPU.  Device step: values assembled on the GPU from the 13 basis vectors
+    of the family (tc_plan_pack_lincomb), factorised, log-determinants handed
+    off device-side.  e2e: api.logdet_many_sharded from host CSC values (H2D
+    per problem) + one NCCL all-gather of the 64 log-determinants."""
+    import torch
+    import torch.distributed as dist
+    from paper_2501_02483_b200 import api, matcore, workloads as W
+    from paper_2501_02483_b200.batch import shard_range
+    fam = W.InlaFamily()
+    thetas = W.c5_thetas()
+    P = len(thetas)
+    lo, hi = shard_range(P, world, rank)
+    L = max(1, a.lanes)
+    opts = api.FactorOptions(tile_size=nt, ordering=a.ordering, occupancy=a.occupancy, concurrent=L,
+                             executor=a.executor)
+    m0 = fam.matrix(*thetas[0])
+    t0 = time.perf_counter()
+    pat = api._pattern_for(m0, opts)
+    setup_s = time.perf_counter() - t0
+    plan = pat.plan
+    F = plan.info()["tile_flops"]
+    coefs = [fam.lincomb(*t)[0] for t in thetas]
+    basis = fam.lincomb(*thetas[0])[1]
+    bd = torch.from_numpy(np.stack([pat.permuted_values(matcore.SymmetricCsc(m0.n, m0.col_ptr, m0.row_idx, b))
+                                    for b in basis])).cuda()
+    offs = pat.offsets()
+    streams = [torch.cuda.Stream() for _ in range(L)]
+    stor = [plan.new_storage() for _ in range(L)]
+    nloc = hi - lo
+    fail = torch.zeros(max(1, nloc), dtype=torch.int64, device="cuda")
+    ld = torch.zeros(max(1, nloc), dtype=torch.float64, device="cuda")
+
+    def step():
+        start = torch.cuda.Event(enable_timing=True)
+        start.record()
+        ends = []
+        for s in streams:
+            s.wait_event(start)
+        for j in range(nloc):
+            lane = j % L
+            s = streams[lane]
+            sh = s.cuda_stream
+            plan.pack_lincomb(bd, coefs[lo + j], offs, stor[lane], sh)
+            plan.factorize_async(stor[lane], lane, sh)
+            plan.copy_result(lane, sh, fail[j:j + 1], ld[j:j + 1])
+        for s in streams:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(s)
+            ends.append(e)
+        return start, ends
+
+    t0 = time.perf_counter()
+    for _ in range(max(a.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    print(f"[c5] warm-up {time.perf_counter() - t0:.1f} s", file=sys.stderr, flush=True)
+    ok = bool((fail[:nloc] == np.iinfo(np.int64).max).all().item()) if nloc else True
+    if not ok:
+        raise RuntimeError("a batch factorisation failed")
+    ld_ref = ld[:nloc].clone()
+    if world > 1:
+        dist.barrier()
+    clk = Clocks(int(os.environ.get("LOCAL_RANK", "0")))
+    clk.start()
+    torch.cuda.synchronize()
+    evs = [step() for _ in range(a.steps)]
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    print(f"[c5] timed steps done", file=sys.stderr, flush=True)
+    ms = evs[0][0].elapsed_time(evs[-1][0]) if a.steps > 1 else 0.0
+    ms = max(evs[-1][0].elapsed_time(e) for e in evs[-1][1]) + ms
+    ms /= a.steps
+    assert torch.equal(ld[:nloc], ld_ref), "timed steps must reproduce the warm-up log-determinants bitwise"
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    # ---- end to end: host values of this rank's problems -> logdet_many_sharded
+    probs = [None] * P
+    for i in range(lo, hi):
+        probs[i] = fam.matrix(*thetas[i])
+    h2d = sum(probs[i].nnz * 8 for i in range(lo, hi))
+    e2e_ms = []
+    for i in range(a.e2e_steps + 1):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        lds = api.logdet_many_sharded(probs, opts, lanes=L)
+        dt = (time.perf_counter() - t0) * 1e3
+        if i > 0:
+            e2e_ms.append(dt)
+    e2e = float(np.mean(e2e_ms)) if e2e_ms else float("nan")
+    if world > 1:
+        t = torch.tensor([e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = float(t.item())
+    assert np.array_equal(lds[lo:hi], ld_ref.cpu().numpy()), "public-API batch must equal the device step bitwise"
+    peak, peak_src = fp64_peak()
+    value = P * 1000.0 / ms
+    line = {"metric": "batched factorizations/s (FP64, C5)", "value": value, "unit": "factorizations/s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": desc, "tile": nt, "n": m0.n, "nnz": m0.nnz, "problems": P,
+                       "lanes_per_gpu": L, "parallelism": f"batch sharded over {world} GPU(s), contiguous blocks",
+                       "l2": "inputs larger than L2 (tile storage %.2f GB per lane)" % (16.0 * nt * nt * plan.S / 2e9)},
+            "roofline": {"bound": "tensor", "kernel": "k_persist x lanes", "achieved": P * F / (ms * 1e-3) / 1e12,
+                         "peak": peak, "unit": "TFLOP/s", "frac": P * F / (ms * 1e-3) / 1e12 / peak,
+                         "traffic": None, "peak_source": peak_src},
+            "gpu_launches": 3 * max(1, nloc), "setup_s": setup_s,
+            "e2e": {"value": P * 1000.0 / e2e, "unit": "factorizations/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(16 * nloc + 8 * P), "ms_per_step": e2e,
+                    "path": "api.logdet_many_sharded(host CSC values)" + (" + NCCL all_gather" if world > 1 else "")},
+            "clocks": clocks}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 # --------------------------------------------------------------- GPU arm --
 def run_ours(a, name, nt, desc, rank, world):
+    if name == "c5":
+        return run_batch(a, nt, desc, rank, world)
     import torch
     import torch.distributed as dist
     from paper_2501_02483_b200 import api
@@ -421,7 +562,8 @@ def run_ours(a, name, nt, desc, rank, world):
                               "hbm_gbs": hbm, "hbm_source": hbm_src},
             "roofline": {"bound": "tensor", "kernel": kname, "achieved": F / (kernel_ms * 1e-3) / 1e12,
                          "peak": peak, "unit": "TFLOP/s", "frac": F / (kernel_ms * 1e-3) / 1e12 / peak,
-                         "traffic": None, "kernel_ms": kernel_ms, "peak_source": peak_src,
+                         "traffic": traffic_of(name, nt)[0], "traffic_source": traffic_of(name, nt)[1],
+                         "kernel_ms": kernel_ms, "peak_source": peak_src,
                          "note": "algorithmic tile flops (SYRK = nt^3, GEMM = 2 nt^3, POTRF = nt^3/3, TRSM = nt^3) "
                                  "per launch / CUDA-event launch time; traffic: see profiles/"},
             "gpu_launches": (1 if a.executor == "persistent" else int(info["launches"])) + 2,
@@ -452,6 +594,9 @@ def _useful_flops(pat):
 
 def main():
     a = parse()
+    if os.environ.get("TC_BENCH_TRACEBACK"):  # debugging hangs: dump the Python stack after N s
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["TC_BENCH_TRACEBACK"]), exit=True)
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -166,8 +166,9 @@ typedef struct tc_plan_opts {
     int32_t tree_threshold; /* chains with accum >= threshold are split; 0 = 2*W, <0 = off */
     int32_t chunk;          /* columns per split-K chunk launch; 0 = auto */
     int32_t lookahead;      /* D >= 1: last D contributing columns split off the bulk update; 0 = off */
-    int32_t use_graph;      /* 1 = CUDA graph (default), 0 = direct stream launches */
-    int32_t reserved[3];
+    int32_t use_graph;      /* 2 = persistent (default), 1 = CUDA graph, 0 = direct launches */
+    int32_t reserved[3];    /* [0] 1 = no POTRF->TRSM streaming, [1] persistent CTAs/SM (0 auto),
+                               [2] concurrent factorisations sharing the GPU (grid share) */
 } tc_plan_opts;
 
 /* Build a plan from the factor tile pattern (slots in (col,row) order, all
@@ -185,6 +186,12 @@ int tc_plan_factorize(tc_plan_t p, double* storage_dev, void* stream, int64_t* f
 int tc_plan_factorize_async(tc_plan_t p, int32_t lane, double* storage_dev, void* stream);
 int tc_plan_collect(tc_plan_t p, int32_t lane, void* stream, int64_t* fail_index,
                     double* logdet);
+/* Debug: the current ticket of a lane's persistent kernel (read while it runs). */
+int tc_plan_debug_ticket(tc_plan_t p, int32_t lane, int32_t* ticket, int32_t* ntasks);
+/* Streaming batches: enqueue on `stream` device copies of the lane's failure
+ * word (INT64_MAX = success, else k*nt+info) and log-determinant. */
+int tc_plan_copy_result(tc_plan_t p, int32_t lane, void* stream, int64_t* fail_dev,
+                        double* logdet_dev);
 /* 2 * sum log diag(L) over non-padding diagonal positions. */
 int tc_plan_logdet(tc_plan_t p, const double* storage_dev, void* stream, double* out);
 /* In-place tile forward/back substitution of rhs_dev[nrhs][T*nt] (column of
@@ -198,6 +205,12 @@ int tc_plan_pack_offsets(tc_plan_t p, int64_t n, const int64_t* col_ptr,
                          const int32_t* row_idx, int64_t* offsets_out);
 int tc_plan_pack(tc_plan_t p, const double* values_dev, const int64_t* offsets_dev,
                  int64_t nnz, double* storage_dev, void* stream);
+/* Device value assembly for a family of matrices sharing the pattern
+ * (INLA batch): storage <- scatter of sum_i coef[i] *
+ * basis_dev[i][0:nnz] (nbasis <= 16, evaluated left to right, products and
+ * sums separately rounded: bitwise the host evaluation of the same sum). */
+int tc_plan_pack_lincomb(tc_plan_t p, const double* basis_dev, int32_t nbasis, const double* coef,
+                         const int64_t* offsets_dev, int64_t nnz, double* storage_dev, void* stream);
 void tc_plan_destroy(tc_plan_t p);
 
 /* Profiling: serialised single-stream pass of the plan with CUDA events around

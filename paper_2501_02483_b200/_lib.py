@@ -79,10 +79,13 @@ SIGNATURES = {
     "tc_plan_factorize": (C.c_int, [vp, vp, vp, i64p]),
     "tc_plan_factorize_async": (C.c_int, [vp, i32, vp, vp]),
     "tc_plan_collect": (C.c_int, [vp, i32, vp, i64p, f64p]),
+    "tc_plan_copy_result": (C.c_int, [vp, i32, vp, vp, vp]),
+    "tc_plan_debug_ticket": (C.c_int, [vp, i32, i32p, i32p]),
     "tc_plan_logdet": (C.c_int, [vp, vp, vp, f64p]),
     "tc_plan_solve": (C.c_int, [vp, vp, vp, i32, vp]),
     "tc_plan_pack_offsets": (C.c_int, [vp, i64, i64p, i32p, i64p]),
     "tc_plan_pack": (C.c_int, [vp, vp, vp, i64, vp, vp]),
+    "tc_plan_pack_lincomb": (C.c_int, [vp, vp, i32, f64p, vp, i64, vp, vp]),
     "tc_plan_destroy": (None, [vp]),
     "tc_plan_profile": (C.c_int, [vp, vp, vp, i32, f64p, i64p, f64p]),
     "tc_plan_trace": (C.c_int, [vp, vp, vp, i64, i64p, i32p, i64, i32p, i64p, i64p]),

@@ -28,7 +28,7 @@ from .scheduler import DevicePlan, PlanOptions
 from .symbolic import TileSymbolic, tile_symbolic_factorize
 
 __all__ = ["FactorOptions", "FactorContext", "factorize", "solve", "logdet", "factorize_many",
-           "factorize_many_sharded", "clear_plan_cache"]
+           "factorize_many_sharded", "logdet_many", "logdet_many_sharded", "clear_plan_cache"]
 
 _ORDERINGS = ("auto", "identity", "partial-rcm", "min-degree", "adaptable-nd")
 _REDUCTIONS = ("auto", "on", "off")
@@ -50,6 +50,7 @@ class FactorOptions:
     executor: str = "persistent"  # persistent | graph | direct
     chunk: int = 0
     occupancy: int = 0             # persistent CTAs per SM (0 auto, 1, 2)
+    concurrent: int = 1            # factorisations meant to share the GPU (batch lanes)
 
     def __post_init__(self):
         if self.tile_size < 1:
@@ -70,7 +71,7 @@ class FactorOptions:
         thr = {"off": -1, "on": 2 * min(W, 16), "auto": 0}[self.tree_reduction]
         return PlanOptions(tree_workers=min(W, 16), tree_threshold=thr, chunk=self.chunk,
                            lookahead=self.lookahead, executor=self.executor,
-                           occupancy=self.occupancy)
+                           occupancy=self.occupancy, concurrent=self.concurrent)
 
 
 @dataclass(eq=False)
@@ -337,3 +338,92 @@ def factorize_many_sharded(problems, rhs=None, opts: FactorOptions | None = None
     return {"logdet": allv[:, 0].copy(),
             "x": [allv[i, 1:].copy() for i in range(P)] if width > 1 else None,
             "local": local}
+
+
+def logdet_many(problems, opts: FactorOptions | None = None, lanes: int = 4) -> np.ndarray:
+    """Streaming batch for the INLA use (SPEC.md:513-519 semantics, results
+    only): log-determinants of independent SPD matrices, ``lanes``
+    factorisations in flight on their own streams, each lane reusing one
+    pinned staging buffer and one device tile storage, results handed off
+    device-side (no per-problem host sync, no factor kept alive).  Each
+    lane's persistent kernel takes 1/lanes of the SMs.  Failures are
+    aggregated into FactorizeManyError; values equal solo factorisations.
+    """
+    import dataclasses
+
+    import torch
+    _lib.require_device()
+    o = opts or FactorOptions()
+    L = max(1, int(lanes))
+    if o.concurrent == 1 and L > 1:
+        o = dataclasses.replace(o, concurrent=L)
+    elif o.concurrent < 1:  # 0: every lane's kernel takes the whole GPU
+        o = dataclasses.replace(o, concurrent=1)
+    items = [p if isinstance(p, SymmetricCsc) else p[0] for p in problems]
+    P = len(items)
+    fail = torch.full((P,), -1, dtype=torch.int64, device="cuda")
+    ld = torch.zeros(P, dtype=torch.float64, device="cuda")
+    streams = [torch.cuda.Stream() for _ in range(L)]
+    staged = [None] * L        # (pinned host, device values, copy-done event) per lane
+    storages: dict = {}        # (pattern id, lane) -> tile storage
+    errors: dict = {}
+    pats = [None] * P
+    for i, m in enumerate(items):
+        lane = i % L
+        s = streams[lane]
+        sh = _stream_handle(s)
+        try:
+            pat = _pattern_for(m, o)
+        except Exception as e:  # noqa: BLE001 - per-problem aggregation
+            errors[i] = e
+            continue
+        pats[i] = pat
+        vals = pat.permuted_values(m)
+        st = staged[lane]
+        if st is None or st[0].numel() < vals.size:
+            st = (torch.empty(vals.size, dtype=torch.float64).pin_memory(),
+                  torch.empty(vals.size, dtype=torch.float64, device="cuda"), torch.cuda.Event())
+            staged[lane] = st
+        else:
+            st[2].synchronize()  # the lane's previous H2D has left the pinned buffer
+        host, dev, ev = st
+        host[: vals.size].copy_(torch.from_numpy(np.ascontiguousarray(vals, dtype=np.float64)))
+        key = (id(pat.plan), lane)
+        if key not in storages:
+            storages[key] = pat.plan.new_storage()
+        with torch.cuda.stream(s):
+            dev[: vals.size].copy_(host[: vals.size], non_blocking=True)
+            ev.record(s)
+            pat.plan.pack(dev[: vals.size], pat.offsets(), storages[key], sh)
+            pat.plan.factorize_async(storages[key], lane, sh)
+            pat.plan.copy_result(lane, sh, fail[i:i + 1], ld[i:i + 1])
+    for s in streams:
+        s.synchronize()
+    f = fail.cpu().numpy()
+    out = ld.cpu().numpy()
+    for i in range(P):
+        if i in errors or pats[i] is None:
+            continue
+        if f[i] != np.iinfo(np.int64).max:
+            idx = int(f[i])
+            m = items[i]
+            orig = int(pats[i].perm.inverse[idx]) if idx < m.n else None
+            errors[i] = NotPositiveDefiniteError(idx, orig)
+            out[i] = np.nan
+    if errors:
+        raise FactorizeManyError(errors, list(out))
+    return out
+
+
+def logdet_many_sharded(problems, opts: FactorOptions | None = None, lanes: int = 4, group=None) -> np.ndarray:
+    """logdet_many over the ranks of a torch.distributed (NCCL) group: rank r
+    streams its contiguous block of problems, then one all-gather of the
+    per-problem log-determinants."""
+    import torch.distributed as dist
+    from .batch import gather_rows, shard_range
+    P = len(problems)
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    lo, hi = shard_range(P, world, rank)
+    local = logdet_many(problems[lo:hi], opts=opts, lanes=lanes) if hi > lo else np.zeros(0)
+    return gather_rows(local.reshape(-1, 1), P, group=group, device="cuda")[:, 0].copy()

@@ -1108,14 +1108,17 @@ int build_persistent(tc_plan& P) {
     // the update pipeline's bubbles
     const int occ_mode = P.opts.reserved[1];
     P.persist_minb = occ_mode == 1 ? 1 : occ_mode == 2 ? 2 : (P.flops / std::max(1, P.T) < 4.0e8 ? 1 : 2);
-    const PersistKernel K = pick_persist(nt, P.persist_minb);
     bool in_smem;
     // shared memory: the max over task kinds; the fused TRSM may stage L
     // strip by strip (ring) instead of whole when that lets two CTAs share an SM
     const size_t xs_bytes = P.nfused ? (size_t)8 * pad_ld((nt + 7) & ~7) * sizeof(double) : 0;
+    const size_t two_per_sm = 108 * 1024;  // (228 KB - reserved - static) / 2
+    if (P.persist_minb == 2 &&
+        std::max<size_t>((size_t)pick_persist(nt, 2).smem, potrf_smem(nt, &in_smem) + xs_bytes) > two_per_sm)
+        P.persist_minb = 1;  // two CTAs cannot share an SM (packed POTRF tile too large): no register cap
+    const PersistKernel K = pick_persist(nt, P.persist_minb);
     const size_t base = std::max<size_t>({(size_t)K.smem, potrf_smem(nt, &in_smem) + xs_bytes, (size_t)4096});
     const size_t t_full = trsm_smem_bytes<kPersistTrsmRows>(nt);
-    const size_t two_per_sm = 108 * 1024;  // (228 KB - reserved - static) / 2
     P.persist_trsm_ring = 0;
     P.persist_smem = std::max(base, t_full);
     if (P.persist_minb == 2 && P.persist_smem > two_per_sm) {
@@ -1135,7 +1138,11 @@ int build_persistent(tc_plan& P) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, K.fn, kPersistThreads, P.persist_smem));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P.dev));
     if (per_sm < 1) return set_err(TC_ERR_CUDA, "persistent kernel does not fit on an SM (smem %zu)", P.persist_smem);
-    P.persist_grid = per_sm * sms;
+    // opts.reserved[2] = number of factorisations meant to run concurrently
+    // (batch lanes): each launch then takes its share of the SMs so the
+    // lanes' persistent kernels coexist instead of serialising
+    const int conc = std::max(1, (int)P.opts.reserved[2]);
+    P.persist_grid = std::max(1, (per_sm * sms) / conc);
     CK(cudaStreamSynchronize(s0));
     return TC_OK;
 }
@@ -1417,8 +1424,11 @@ extern "C" int tc_plan_factorize_async(tc_plan_t p, int32_t lane, double* storag
     ln.h.ld_part = ln.d_ld;
     ln.h.ld_out = ln.d_ld + p->T;
     const int64_t nf = kNoFail;
-    CK(cudaMemcpyAsync(ln.d_ctx, &ln.h, sizeof(Ctx), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(ln.d_fail, &nf, 8, cudaMemcpyHostToDevice, s));
+    // context + failure word set by a 1-thread kernel: the values travel as
+    // launch parameters (no pageable host source whose lifetime or staging
+    // semantics could race with the lane's next call)
+    k_set_ctx<<<1, 1, 0, s>>>(ln.d_ctx, ln.h, ln.d_fail, nf);
+    CK(cudaGetLastError());
     if (p->opts.use_graph == 2) {
         r = run_persistent(*p, ln, s);
         if (r) return r;
@@ -1445,6 +1455,61 @@ extern "C" int tc_plan_collect(tc_plan_t p, int32_t lane, void* stream, int64_t*
     CK(cudaStreamSynchronize(s));
     if (fail_index) *fail_index = (f == kNoFail) ? -1 : f;
     if (logdet) *logdet = ld;
+    return TC_OK;
+}
+
+// Debug: current ticket of a lane's running persistent kernel (copied on a
+// private non-blocking stream, so it can be read while the kernel spins).
+extern "C" int tc_plan_debug_ticket(tc_plan_t p, int32_t lane, int32_t* ticket, int32_t* ntasks) {
+    if (!p || lane < 0 || lane >= (int)p->lanes.size() || !p->lanes[lane].d_pstate)
+        return set_err(TC_ERR_ARG, "plan_debug_ticket: bad lane");
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const size_t NL = p->launches.size();
+    CK(cudaMemcpyAsync(ticket, p->lanes[lane].d_pstate + 2 * NL, 4, cudaMemcpyDeviceToHost, s));
+    if (getenv("TC_DEBUG_DUMP")) {  // remaining/deps + ticket order of every launch -> file
+        std::vector<int32_t> st(2 * NL);
+        CK(cudaMemcpyAsync(st.data(), p->lanes[lane].d_pstate, 2 * NL * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        char fn[512];
+        snprintf(fn, sizeof fn, "%s.%d", getenv("TC_DEBUG_DUMP"), lane);
+        FILE* f = fopen(fn, "w");
+        std::vector<int64_t> first(NL, -1);
+        for (size_t t = 0; t < p->ptasks.size(); ++t)
+            if (first[p->ptasks[t].launch] < 0) first[p->ptasks[t].launch] = (int64_t)t;
+        for (size_t i = 0; i < NL; ++i)
+            fprintf(f, "%zu %d %d %d %d %lld\n", i, p->launches[i].kind, p->launches[i].k, st[i], st[NL + i],
+                    (long long)first[i]);
+        fclose(f);
+        std::vector<int32_t> pr(p->T, -7);
+        int64_t fw = 0;
+        if (p->lanes[lane].d_prog)
+            CK(cudaMemcpyAsync(pr.data(), p->lanes[lane].d_prog, p->T * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&fw, p->lanes[lane].d_fail, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        snprintf(fn, sizeof fn, "%s.%d.prog", getenv("TC_DEBUG_DUMP"), lane);
+        f = fopen(fn, "w");
+        fprintf(f, "fail %lld\n", (long long)fw);
+        for (int k = 0; k < p->T; ++k) fprintf(f, "%d %d\n", k, pr[k]);
+        fclose(f);
+    }
+    CK(cudaStreamSynchronize(s));
+    cudaStreamDestroy(s);
+    *ntasks = (int32_t)p->ptasks.size();
+    return TC_OK;
+}
+
+// Asynchronous result hand-off for streaming batches: enqueue device-to-device
+// copies of a lane's failure word (kNoFail = INT64_MAX when the factorisation
+// succeeded) and log-determinant into caller buffers, so the lane can take the
+// next problem without a host round trip.
+extern "C" int tc_plan_copy_result(tc_plan_t p, int32_t lane, void* stream, int64_t* fail_dev, double* logdet_dev) {
+    if (!p || lane < 0 || lane >= (int)p->lanes.size() || !p->lanes[lane].d_ctx)
+        return set_err(TC_ERR_ARG, "plan_copy_result: bad lane");
+    Lane& ln = p->lanes[lane];
+    cudaStream_t s = (cudaStream_t)stream;
+    if (fail_dev) CK(cudaMemcpyAsync(fail_dev, ln.d_fail, 8, cudaMemcpyDeviceToDevice, s));
+    if (logdet_dev) CK(cudaMemcpyAsync(logdet_dev, ln.d_ld + p->T, 8, cudaMemcpyDeviceToDevice, s));
     return TC_OK;
 }
 
@@ -1522,6 +1587,26 @@ extern "C" int tc_plan_pack_offsets(tc_plan_t p, int64_t n, const int64_t* col_p
     return TC_OK;
 }
 
+extern "C" int tc_plan_pack_lincomb(tc_plan_t p, const double* basis, int32_t nbasis, const double* coef,
+                                    const int64_t* offs, int64_t nnz, double* storage, void* stream) {
+    if (!p || !storage || !coef || nbasis < 1 || nbasis > kMaxBasis || (nnz > 0 && (!basis || !offs)))
+        return set_err(TC_ERR_ARG, "plan_pack_lincomb: bad arguments (1 <= nbasis <= %d)", kMaxBasis);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t bytes = (size_t)p->S * p->nt * p->nt * sizeof(double);
+    CK(cudaMemsetAsync(storage, 0, bytes, s));
+    if (nnz > 0) {
+        Lincomb lc{};
+        lc.m = nbasis;
+        for (int i = 0; i < nbasis; ++i) lc.c[i] = coef[i];
+        const int64_t blocks = std::min<int64_t>((nnz + 255) / 256, 148 * 16);
+        k_pack_lincomb<<<(unsigned)blocks, 256, 0, s>>>(basis, nnz, lc, offs, storage);
+    }
+    const int from = (int)(p->n % p->nt);
+    if (from) k_pad_diag<<<1, p->nt, 0, s>>>(storage, p->cs[p->T - 1], p->nt, from);
+    CK(cudaGetLastError());
+    return TC_OK;
+}
+
 extern "C" int tc_plan_pack(tc_plan_t p, const double* vals, const int64_t* offs, int64_t nnz, double* storage,
                             void* stream) {
     if (!p || !storage || (nnz > 0 && (!vals || !offs))) return set_err(TC_ERR_ARG, "plan_pack: bad arguments");
@@ -1591,8 +1676,11 @@ extern "C" int tc_plan_profile(tc_plan_t p, double* storage, void* stream, int32
     ln.h.ld_part = ln.d_ld;
     ln.h.ld_out = ln.d_ld + p->T;
     const int64_t nf = kNoFail;
-    CK(cudaMemcpyAsync(ln.d_ctx, &ln.h, sizeof(Ctx), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(ln.d_fail, &nf, 8, cudaMemcpyHostToDevice, s));
+    // context + failure word set by a 1-thread kernel: the values travel as
+    // launch parameters (no pageable host source whose lifetime or staging
+    // semantics could race with the lane's next call)
+    k_set_ctx<<<1, 1, 0, s>>>(ln.d_ctx, ln.h, ln.d_fail, nf);
+    CK(cudaGetLastError());
     const size_t NL = p->launches.size();
     std::vector<cudaEvent_t> ev(NL + 1);
     for (auto& e : ev) CK(cudaEventCreate(&e));

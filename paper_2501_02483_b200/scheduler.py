@@ -41,6 +41,7 @@ class PlanOptions:
     executor: str = "persistent"  # persistent | graph | direct
     occupancy: int = 0            # persistent CTAs per SM: 0 auto (2 when it fits), 1, 2
     fuse_trsm: bool = True        # persistent: TRSM(k) streams POTRF(k)'s panels
+    concurrent: int = 1           # persistent: factorisations sharing the GPU (grid share)
 
     def to_c(self) -> PlanOpts:
         o = PlanOpts()
@@ -51,6 +52,7 @@ class PlanOptions:
         o.use_graph = {"direct": 0, "graph": 1, "persistent": 2}[self.executor]
         o.reserved[0] = 0 if self.fuse_trsm else 1
         o.reserved[1] = int(self.occupancy)
+        o.reserved[2] = int(self.concurrent)
         return o
 
 
@@ -104,6 +106,14 @@ class DevicePlan:
             self._offsets = {key: off}
         return off
 
+    def pack_lincomb(self, basis_dev, coef, offsets_dev, storage, stream: int) -> None:
+        """storage <- scatter of sum_i coef[i] * basis_dev[i] (device value
+        assembly of one member of a matrix family on this pattern)."""
+        c = np.ascontiguousarray(np.asarray(coef, dtype=np.float64))
+        check("tc_plan_pack_lincomb", lib.tc_plan_pack_lincomb(
+            self.h, basis_dev.data_ptr(), int(basis_dev.shape[0]), ptr(c, f64p), offsets_dev.data_ptr(),
+            int(basis_dev.shape[1]), storage.data_ptr(), stream))
+
     def pack(self, values_dev, offsets_dev, storage, stream: int) -> None:
         """Zero storage, scatter values (device), unit-pad the last diagonal."""
         check("tc_plan_pack", lib.tc_plan_pack(self.h, values_dev.data_ptr(), offsets_dev.data_ptr(),
@@ -112,6 +122,12 @@ class DevicePlan:
     # ---- numeric phase --------------------------------------------------
     def factorize_async(self, storage, lane: int, stream: int) -> None:
         check("tc_plan_factorize_async", lib.tc_plan_factorize_async(self.h, lane, storage.data_ptr(), stream))
+
+    def copy_result(self, lane: int, stream: int, fail_dev, logdet_dev) -> None:
+        """Enqueue device copies of the lane's failure word / log-determinant
+        (int64 / float64 device tensors of one element, e.g. views into a batch array)."""
+        check("tc_plan_copy_result", lib.tc_plan_copy_result(self.h, lane, stream, fail_dev.data_ptr(),
+                                                             logdet_dev.data_ptr()))
 
     def collect(self, lane: int, stream: int):
         f = np.zeros(1, dtype=np.int64)

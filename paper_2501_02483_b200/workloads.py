@@ -141,6 +141,20 @@ class InlaFamily:
                 v = v + (s * ct[i] * cs[j]) * self.basis[(i, j)]
         return v
 
+    def lincomb(self, kappa: float, rho: float, tau: float):
+        """(coefficients, basis vectors) with values(theta) == the left-to-right
+        sum of coef[i] * basis[i] (separately rounded products and sums; the
+        unit coefficients are exact), for device-side assembly
+        (tc_plan_pack_lincomb)."""
+        k2 = kappa * kappa
+        cs = [k2 * k2, 2.0 * k2, 1.0]
+        ct = [1.0, rho * rho, -rho]
+        s = 1.0 / (1.0 - rho * rho)
+        coef = [1.0, 1.0, 1.0, tau] + [s * ct[i] * cs[j] for i in range(3) for j in range(3)]
+        basis = [self.v_ident, self.v_x, self.v_xtx, self.v_tau] + [self.basis[(i, j)] for i in range(3)
+                                                                      for j in range(3)]
+        return coef, basis
+
     def matrix(self, kappa: float, rho: float, tau: float) -> SymmetricCsc:
         return SymmetricCsc(self.n, self.col_ptr, self.row_idx, self.values(kappa, rho, tau))
 

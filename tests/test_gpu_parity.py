@@ -338,7 +338,7 @@ def _vs_oracle(m, nt, **opts):
     assert abs(api.logdet(ctx) - ld_ref) <= LOGDET_TOL * abs(ld_ref)
 
 
-@pytest.mark.parametrize("nt", [40, 64, 120])
+@pytest.mark.parametrize("nt", [40, 64, 120, 160, 240])
 @pytest.mark.parametrize("occ", [1, 2])
 def test_inla_small_with_fill(torch, nt, occ):
     """Small INLA precision (block-tridiagonal + arrow, fill tiles) through the
@@ -353,3 +353,37 @@ def test_variable_band_small(torch, occ):
     from paper_2501_02483_b200 import workloads as W
     m = W.c2_variable_band(n=6000, t=40, seg_len=600, max_band=300)
     _vs_oracle(m, 48, ordering="identity", occupancy=occ)
+
+
+def test_inla_batch_device_assembly_and_streaming_logdets(torch):
+    """C5 machinery on a small INLA family: device value assembly
+    (tc_plan_pack_lincomb) is bitwise the host values; the streaming batch
+    (logdet_many, lanes sharing the GPU) reproduces solo log-determinants
+    bitwise and aggregates a failing member without cancelling the others."""
+    from paper_2501_02483_b200 import workloads as W
+    from paper_2501_02483_b200.errors import FactorizeManyError, NotPositiveDefiniteError
+    api, ctsf, matcore, symbolic, impl = _imports()
+    fam = W.InlaFamily(nx=10, ny=12, nsteps=20, nfix=3)
+    thetas = W.c5_thetas()[::11]
+    ms = [fam.matrix(*t) for t in thetas]
+    opts = api.FactorOptions(tile_size=64)
+    solo = np.array([api.logdet(api.factorize(m, opts)) for m in ms])
+    many = api.logdet_many(ms, opts, lanes=3)
+    assert np.array_equal(solo, many)
+    pat = api._pattern_for(ms[0], opts)
+    plan = pat.plan
+    offs = pat.offsets()
+    sh = torch.cuda.current_stream().cuda_stream
+    for t, m in zip(thetas, ms):
+        coef, basis = fam.lincomb(*t)
+        bd = torch.from_numpy(np.stack([pat.permuted_values(matcore.SymmetricCsc(m.n, m.col_ptr, m.row_idx, b))
+                                        for b in basis])).cuda()
+        s1, s2 = plan.new_storage(), plan.new_storage()
+        plan.pack_lincomb(bd, coef, offs, s1, sh)
+        plan.pack(torch.from_numpy(np.ascontiguousarray(pat.permuted_values(m))).cuda(), offs, s2, sh)
+        assert torch.equal(s1, s2)
+    bad = matcore.SymmetricCsc(ms[1].n, ms[1].col_ptr, ms[1].row_idx, -ms[1].values)
+    with pytest.raises(FactorizeManyError) as ei:
+        api.logdet_many([ms[0], bad, ms[2]], opts, lanes=2)
+    assert set(ei.value.errors) == {1} and isinstance(ei.value.errors[1], NotPositiveDefiniteError)
+    assert ei.value.results[0] == solo[0] and ei.value.results[2] == solo[2]

@@ -160,3 +160,17 @@ def test_factor_column_counts_sum_to_fill(name):
             below = k + 1 + np.flatnonzero(S[k + 1:, k])
             S[np.ix_(below, below)] = True
         assert np.array_equal(ordering.factor_column_counts(m), np.tril(S).sum(axis=0))
+
+
+def test_inla_lincomb_is_bitwise_values():
+    """Device value assembly contract: the family's (coef, basis) sequence
+    evaluated left to right reproduces values(theta) bitwise."""
+    from paper_2501_02483_b200 import workloads as W
+    fam = W.InlaFamily(nx=6, ny=7, nsteps=5, nfix=2)
+    for th in W.c5_thetas()[::7]:
+        coef, basis = fam.lincomb(*th)
+        assert len(coef) == len(basis) <= 16
+        v = coef[0] * basis[0]
+        for c, b in zip(coef[1:], basis[1:]):
+            v = v + c * b
+        assert np.array_equal(v, fam.values(*th))
