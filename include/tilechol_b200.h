@@ -186,6 +186,11 @@ int tc_plan_factorize(tc_plan_t p, double* storage_dev, void* stream, int64_t* f
 int tc_plan_factorize_async(tc_plan_t p, int32_t lane, double* storage_dev, void* stream);
 int tc_plan_collect(tc_plan_t p, int32_t lane, void* stream, int64_t* fail_index,
                     double* logdet);
+/* End-to-end host staging: page-lock a host array in place (cudaHostRegister)
+ * / release it; async H2D copy on `stream`. */
+int tc_host_register(void* ptr, size_t bytes);
+int tc_host_unregister(void* ptr);
+int tc_memcpy_h2d_async(void* dst_dev, const void* src_host, size_t bytes, void* stream);
 /* Debug: the current ticket of a lane's persistent kernel (read while it runs). */
 int tc_plan_debug_ticket(tc_plan_t p, int32_t lane, int32_t* ticket, int32_t* ntasks);
 /* Streaming batches: enqueue on `stream` device copies of the lane's failure

@@ -81,6 +81,9 @@ SIGNATURES = {
     "tc_plan_collect": (C.c_int, [vp, i32, vp, i64p, f64p]),
     "tc_plan_copy_result": (C.c_int, [vp, i32, vp, vp, vp]),
     "tc_plan_debug_ticket": (C.c_int, [vp, i32, i32p, i32p]),
+    "tc_host_register": (C.c_int, [vp, C.c_size_t]),
+    "tc_host_unregister": (C.c_int, [vp]),
+    "tc_memcpy_h2d_async": (C.c_int, [vp, vp, C.c_size_t, vp]),
     "tc_plan_logdet": (C.c_int, [vp, vp, vp, f64p]),
     "tc_plan_solve": (C.c_int, [vp, vp, vp, i32, vp]),
     "tc_plan_pack_offsets": (C.c_int, [vp, i64, i64p, i32p, i64p]),

@@ -202,13 +202,46 @@ def _stream_handle(stream) -> int:
     return stream.cuda_stream
 
 
+# host arrays page-locked in place (cudaHostRegister), most recent last; the
+# entries hold a reference so the memory stays valid while registered
+_REGISTERED: "OrderedDict[tuple, np.ndarray]" = OrderedDict()
+_REGISTERED_CAP = 16 << 30
+
+
+def _registered(vals: np.ndarray) -> bool:
+    """Page-lock a caller-owned values array once (keyed by address/size);
+    repeated factorisations of the same host matrix (INLA iterations, the
+    bench's e2e loop) then copy at pinned bandwidth with no staging copy."""
+    key = (vals.ctypes.data, vals.nbytes)
+    if key in _REGISTERED:
+        _REGISTERED.move_to_end(key)
+        return True
+    while _REGISTERED and sum(a.nbytes for a in _REGISTERED.values()) + vals.nbytes > _REGISTERED_CAP:
+        (p, _), _a = _REGISTERED.popitem(last=False)
+        _lib.lib.tc_host_unregister(_lib.C.c_void_p(p))
+    if _lib.lib.tc_host_register(_lib.C.c_void_p(key[0]), key[1]) != _lib.TC_OK:
+        return False
+    _REGISTERED[key] = vals
+    return True
+
+
 def _launch(pat: _Pattern, m: SymmetricCsc, lane: int, stream, storage=None):
     """H2D values, device scatter, async factorisation on `stream`."""
     import torch
     vals = np.ascontiguousarray(pat.permuted_values(m), dtype=np.float64)
-    host = torch.from_numpy(vals).pin_memory() if vals.nbytes > (1 << 20) else torch.from_numpy(vals)
+    in_place = vals is m.values and vals.nbytes > (1 << 20) and _registered(vals)
+    if in_place:
+        host = vals
+    else:
+        host = torch.from_numpy(vals).pin_memory() if vals.nbytes > (1 << 20) else torch.from_numpy(vals)
     with torch.cuda.stream(stream):
-        dev = host.to("cuda", non_blocking=True)
+        if in_place:
+            dev = torch.empty(vals.size, dtype=torch.float64, device="cuda")
+            _lib.check("tc_memcpy_h2d_async", _lib.lib.tc_memcpy_h2d_async(
+                _lib.C.c_void_p(dev.data_ptr()), _lib.C.c_void_p(vals.ctypes.data), vals.nbytes,
+                _lib.C.c_void_p(_stream_handle(stream))))
+        else:
+            dev = host.to("cuda", non_blocking=True)
         if storage is None:
             storage = pat.plan.new_storage()
         pat.plan.pack(dev, pat.offsets(), storage, _stream_handle(stream))

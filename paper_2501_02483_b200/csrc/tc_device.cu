@@ -1651,6 +1651,25 @@ extern "C" void tc_plan_destroy(tc_plan_t p) {
     delete p;
 }
 
+// Host staging for the end-to-end path: page-lock a caller's host array in
+// place (no copy) so its per-call H2D runs at pinned bandwidth, and an async
+// copy that does not depend on the caller knowing the pointer is registered.
+extern "C" int tc_host_register(void* ptr, size_t bytes) {
+    if (!ptr || !bytes) return set_err(TC_ERR_ARG, "host_register: bad arguments");
+    CK(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
+    return TC_OK;
+}
+extern "C" int tc_host_unregister(void* ptr) {
+    if (!ptr) return set_err(TC_ERR_ARG, "host_unregister: null");
+    CK(cudaHostUnregister(ptr));
+    return TC_OK;
+}
+extern "C" int tc_memcpy_h2d_async(void* dst_dev, const void* src_host, size_t bytes, void* stream) {
+    if (!dst_dev || !src_host) return set_err(TC_ERR_ARG, "memcpy_h2d_async: bad arguments");
+    CK(cudaMemcpyAsync(dst_dev, src_host, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+    return TC_OK;
+}
+
 // error hook shared with the host-analysis translation unit (tc_host.cpp)
 extern "C" int tc__set_error(int code, const char* msg) {
     g_err = msg;
