@@ -78,31 +78,57 @@ UpdKernel pick_upd(int nt) {
     return mk_upd<32, 32, 2, 2, 1>();
 }
 
+// Small square blocks for the one-pair L(k) items on the critical path: a
+// 40x40x120 block costs ~7 us on one SM (8-way split-K tree epilogue
+// included); 24x24 spreads the same GEMM over ~3x more SMs at ~1/3 the
+// per-CTA work.  0 = none (tile size not a multiple of 24 or 32).
+int small_block(int nt) {
+    if (getenv("TC_NO_SMALL_LAST")) return 0;
+    if (nt % 24 == 0 && nt >= 96) return 24;
+    if (nt % 32 == 0 && nt >= 96) return 32;
+    return 0;
+}
+UpdKernel pick_upd_small(int nt) {
+    switch (small_block(nt)) {
+        case 24: return mk_upd<24, 24, 1, 1, 4>();
+        case 32: return mk_upd<32, 32, 1, 1, 4>();
+        default: return UpdKernel{};
+    }
+}
+
 struct PersistKernel {
     void (*fn)(PersistArgs);
     int BM, BN, smem;
 };
 
+template <int BM, int BN, int WGM, int WGN, int KS, int SB>
+PersistKernel mk_persist_sb(int minb) {
+    return PersistKernel{minb == 2 ? k_persist<BM, BN, WGM, WGN, KS, 2, SB> : k_persist<BM, BN, WGM, WGN, KS, 1, SB>,
+                         BM, BN, UpdCfg<BM, BN, WGM, WGN, KS>::SMEM};
+}
 template <int BM, int BN, int WGM, int WGN, int KS>
-PersistKernel mk_persist(int minb) {
-    return PersistKernel{minb == 2 ? k_persist<BM, BN, WGM, WGN, KS, 2> : k_persist<BM, BN, WGM, WGN, KS, 1>, BM, BN,
-                         UpdCfg<BM, BN, WGM, WGN, KS>::SMEM};
+PersistKernel mk_persist(int minb, int nt) {
+    switch (small_block(nt)) {
+        case 24: return mk_persist_sb<BM, BN, WGM, WGN, KS, 24>(minb);
+        case 32: return mk_persist_sb<BM, BN, WGM, WGN, KS, 32>(minb);
+        default: return mk_persist_sb<BM, BN, WGM, WGN, KS, 0>(minb);
+    }
 }
 
 // same block shapes as pick_upd, 256-thread variants (KSPLIT doubled);
 // minb = minimum resident CTAs per SM the variant is compiled for
 PersistKernel pick_persist(int nt, int minb) {
     if (const char* f = getenv("TC_PERSIST_SHAPE")) {  // tuning override
-        if (!strcmp(f, "64")) return mk_persist<64, 64, 2, 2, 2>(minb);
-        if (!strcmp(f, "32")) return mk_persist<32, 32, 2, 2, 2>(minb);
-        if (!strcmp(f, "40")) return mk_persist<40, 40, 1, 1, 8>(minb);
+        if (!strcmp(f, "64")) return mk_persist<64, 64, 2, 2, 2>(minb, nt);
+        if (!strcmp(f, "32")) return mk_persist<32, 32, 2, 2, 2>(minb, nt);
+        if (!strcmp(f, "40")) return mk_persist<40, 40, 1, 1, 8>(minb, nt);
     }
-    if (nt % 64 == 0) return mk_persist<64, 64, 2, 2, 2>(minb);
-    if (nt % 80 == 0 && nt % 48 == 0) return mk_persist<80, 48, 2, 2, 2>(minb);
-    if (nt % 80 == 0) return mk_persist<80, 40, 2, 1, 4>(minb);
-    if (nt % 40 == 0) return mk_persist<40, 40, 1, 1, 8>(minb);
-    if (nt >= 96) return mk_persist<64, 64, 2, 2, 2>(minb);
-    return mk_persist<32, 32, 2, 2, 2>(minb);
+    if (nt % 64 == 0) return mk_persist<64, 64, 2, 2, 2>(minb, nt);
+    if (nt % 80 == 0 && nt % 48 == 0) return mk_persist<80, 48, 2, 2, 2>(minb, nt);
+    if (nt % 80 == 0) return mk_persist<80, 40, 2, 1, 4>(minb, nt);
+    if (nt % 40 == 0) return mk_persist<40, 40, 1, 1, 8>(minb, nt);
+    if (nt >= 96) return mk_persist<64, 64, 2, 2, 2>(minb, nt);
+    return mk_persist<32, 32, 2, 2, 2>(minb, nt);
 }
 
 int prep_kernel(const void* fn, int smem) {
@@ -490,6 +516,7 @@ struct Launch {
     int64_t scratch0 = 0;        // COMBINE
     uint32_t live = 0;           // COMBINE
     int cls = 0;                 // profiling class: 0 bulk, 1 last, 2 potrf, 3 trsm, 4 combine, 5 logdet, 6 split-K chunk
+    int small = 0;               // UPD items use the small latency block (L(k) launches)
     double flops = 0.0;          // algorithmic flops of this launch
     std::vector<int32_t> deps;
 };
@@ -526,6 +553,7 @@ struct tc_plan {
     int64_t R = 0;                      // scratch tiles per lane
     double flops = 0.0;
     UpdKernel upd{};
+    UpdKernel upd_small{};              // L(k): one-pair items in small blocks (latency), fn == null if none
     // device copies
     Item* d_items = nullptr;
     Pair* d_pairs = nullptr;
@@ -539,7 +567,7 @@ struct tc_plan {
     int prio_hi = 0, prio_lo = 0;
     int dev = 0;
     // per-column launch ids (persistent ticket order)
-    std::vector<int32_t> colB, colM, colL, colPot, colTrsm;
+    std::vector<int32_t> colB, colM, colL, colLo, colPot, colTrsm;
     std::vector<std::vector<int32_t>> colComb, colChunk;
     // persistent executor
     std::vector<PTask> ptasks;
@@ -669,6 +697,7 @@ int build_plan(tc_plan& P) {
     P.colB.assign(T, -1);
     P.colM.assign(T, -1);
     P.colL.assign(T, -1);
+    P.colLo.assign(T, -1);
     P.colPot.assign(T, -1);
     P.colTrsm.assign(T, -1);
     P.colComb.assign(T, {});
@@ -690,8 +719,16 @@ int build_plan(tc_plan& P) {
         }
     };
 
+    std::vector<std::pair<int, int>> sblk_full, sblk_low;
+    const int SBK = (P.opts.use_graph == 2 || P.opts.use_graph == 0 || P.opts.use_graph == 1) ? small_block(nt) : 0;
+    if (SBK) {
+        tile_blocks(nt, SBK, SBK, false, sblk_full);
+        tile_blocks(nt, SBK, SBK, true, sblk_low);
+    }
+    bool small_now = false;  // emitting an L(k) launch
     auto emit_items = [&](int64_t t, int64_t p0, int64_t p1, int32_t dst, int mode) {
-        for (auto& bl : blocks_for(t))
+        const auto& bl_list = (small_now && SBK) ? (P.frow[t] == P.fcol[t] ? sblk_low : sblk_full) : blocks_for(t);
+        for (auto& bl : bl_list)
             P.items.push_back(Item{dst, bl.first, bl.second, (int32_t)p0, (int32_t)p1, mode});
     };
 
@@ -761,28 +798,47 @@ int build_plan(tc_plan& P) {
             }
         }
         const int32_t prev = mnode >= 0 ? mnode : bnode;  // last writer of column k before L(k)
+        // L(k): the last contribution.  With small blocks available it is split
+        // into L_diag(k) (the diagonal tile, small blocks: POTRF(k) waits only
+        // on it) and L_off(k) (off-diagonal targets, regular blocks: only
+        // TRSM(k) waits on them, and TRSM streams behind POTRF anyway)
+        int32_t lnode_off = -1;
         if (nlast >= 0) {
-            Launch L;
-            L.kind = L_UPD;
-            L.k = k;
-            L.high = 1;
-            L.cls = 1;
-            L.off = (int64_t)P.items.size();
-            for (int64_t t = c0; t < c1; ++t) {
-                if (red_base[t] >= 0) continue;
-                const int64_t p1 = tp1[t];
-                if (p1 > tp0[t] && P.fcol[P.pairs[p1 - 1].b] == nlast) {
-                    emit_items(t, p1 - 1, p1, (int32_t)t, MODE_SUB);
-                    L.flops += (P.frow[t] == k ? 1.0 : 2.0) * n3;
+            for (int part = 0; part < 2; ++part) {
+                const bool diag_part = part == 0;
+                if (!SBK && !diag_part) break;  // unsplit: one launch, regular blocks
+                Launch L;
+                L.kind = L_UPD;
+                L.k = k;
+                L.high = 1;
+                L.cls = 1;
+                L.off = (int64_t)P.items.size();
+                small_now = SBK != 0 && diag_part;
+                L.small = small_now ? 1 : 0;
+                for (int64_t t = c0; t < c1; ++t) {
+                    if (red_base[t] >= 0) continue;
+                    if (SBK && ((t == c0) != diag_part)) continue;
+                    const int64_t p1 = tp1[t];
+                    if (p1 > tp0[t] && P.fcol[P.pairs[p1 - 1].b] == nlast) {
+                        emit_items(t, p1 - 1, p1, (int32_t)t, MODE_SUB);
+                        L.flops += (P.frow[t] == k ? 1.0 : 2.0) * n3;
+                    }
                 }
-            }
-            L.cnt = (int64_t)P.items.size() - L.off;
-            if (L.cnt > 0) {
-                L.deps.push_back(pnode[nlast]);
-                if (prev >= 0) L.deps.push_back(prev);
-                lnode = (int32_t)P.launches.size();
-                P.colL[k] = lnode;
-                P.launches.push_back(std::move(L));
+                small_now = false;
+                L.cnt = (int64_t)P.items.size() - L.off;
+                if (L.cnt > 0) {
+                    L.deps.push_back(pnode[nlast]);
+                    if (prev >= 0) L.deps.push_back(prev);
+                    const int32_t id = (int32_t)P.launches.size();
+                    if (diag_part) {
+                        lnode = id;
+                        P.colL[k] = id;
+                    } else {
+                        lnode_off = id;
+                        P.colLo[k] = id;
+                    }
+                    P.launches.push_back(std::move(L));
+                }
             }
         }
         // combines of reduced targets of this column
@@ -836,6 +892,7 @@ int build_plan(tc_plan& P) {
             if (bnode >= 0) L.deps.push_back(bnode);
             if (mnode >= 0) L.deps.push_back(mnode);
             if (lnode >= 0) L.deps.push_back(lnode);
+            if (lnode_off >= 0) L.deps.push_back(lnode_off);
             for (int32_t x : comb_off) L.deps.push_back(x);
             L.flops += n3 * (double)(c1 - c0 - 1);
             pnode[k] = (int32_t)P.launches.size();
@@ -1000,6 +1057,7 @@ int build_persistent(tc_plan& P) {
         put(P.colL[k]);
         for (int32_t c : P.colComb[k]) put(c);
         put(P.colPot[k]);
+        put(P.colLo[k]);
         if (fuse) put(P.colTrsm[k]);
         if (k + D < T) put(P.colB[k + D]);
         if (k + 1 < T) put(P.colB[k + 1]);
@@ -1033,7 +1091,8 @@ int build_persistent(tc_plan& P) {
         }
         switch (L.kind) {
             case L_UPD:
-                for (int64_t x = loff[id]; x < loff[id] + lcnt[id]; ++x) P.ptasks.push_back(PTask{id, (int32_t)x, 0});
+                for (int64_t x = loff[id]; x < loff[id] + lcnt[id]; ++x)
+                    P.ptasks.push_back(PTask{id, (int32_t)x, L.small});
                 break;
             case L_TRSM:
                 for (int64_t x = L.off; x < L.off + L.cnt; ++x)
@@ -1219,10 +1278,11 @@ int node_params(tc_plan& P, Lane& ln, size_t i, cudaKernelNodeParams& kp, NodeAr
             na.ua.nt = nt;
             na.ua.item_base = (int32_t)L.off;
             argv[0] = &na.ua;
-            kp.func = (void*)P.upd.fn;
+            const UpdKernel& K = (L.small && P.upd_small.fn) ? P.upd_small : P.upd;
+            kp.func = (void*)K.fn;
             kp.gridDim = dim3((unsigned)L.cnt);
-            kp.blockDim = dim3(P.upd.nth);
-            kp.sharedMemBytes = P.upd.smem;
+            kp.blockDim = dim3(K.nth);
+            kp.sharedMemBytes = K.smem;
             break;
         }
         case L_POTRF: {
@@ -1311,6 +1371,7 @@ int ensure_lane(tc_plan& P, int lane) {
 
 int prep_all(tc_plan& P) {
     int r = prep_kernel((const void*)P.upd.fn, P.upd.smem);
+    if (!r && P.upd_small.fn) r = prep_kernel((const void*)P.upd_small.fn, P.upd_small.smem);
     if (r) return r;
     bool in_smem;
     r = prep_kernel((const void*)k_potrf, (int)potrf_smem(P.nt, &in_smem));
@@ -1389,6 +1450,7 @@ extern "C" int tc_plan_create(int64_t n, int32_t nt, int64_t S, const int32_t* f
     P->frow.assign(f_rows, f_rows + S);
     P->fcol.assign(f_cols, f_cols + S);
     P->upd = pick_upd(nt);
+    P->upd_small = pick_upd_small(nt);
     CK(cudaGetDevice(&P->dev));
     CK(cudaDeviceGetStreamPriorityRange(&P->prio_lo, &P->prio_hi));
     int r = build_plan(*P);
