@@ -316,6 +316,8 @@ def factorize_many(problems, opts: FactorOptions | None = None, lanes: int = 4) 
     items = [(p, opts or FactorOptions()) if isinstance(p, SymmetricCsc) else (p[0], p[1] or opts or FactorOptions())
              for p in problems]
     streams = [torch.cuda.Stream() for _ in range(max(1, lanes))]
+    for s in streams:
+        s.wait_stream(torch.cuda.current_stream())
     results: list = [None] * len(items)
     errors: dict = {}
     pending = []
@@ -397,6 +399,8 @@ def logdet_many(problems, opts: FactorOptions | None = None, lanes: int = 4) -> 
     fail = torch.full((P,), -1, dtype=torch.int64, device="cuda")
     ld = torch.zeros(P, dtype=torch.float64, device="cuda")
     streams = [torch.cuda.Stream() for _ in range(L)]
+    for s in streams:  # the result arrays' fill kernels run on the current stream first
+        s.wait_stream(torch.cuda.current_stream())
     staged = [None] * L        # (pinned host, device values, copy-done event) per lane
     storages: dict = {}        # (pattern id, lane) -> tile storage
     errors: dict = {}

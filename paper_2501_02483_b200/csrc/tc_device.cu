@@ -8,6 +8,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "tc_kernels.cuh"
@@ -106,29 +107,29 @@ PersistKernel mk_persist_sb(int minb) {
     return PersistKernel{minb == 2 ? k_persist<BM, BN, WGM, WGN, KS, 2, SB> : k_persist<BM, BN, WGM, WGN, KS, 1, SB>,
                          BM, BN, UpdCfg<BM, BN, WGM, WGN, KS>::SMEM};
 }
-template <int BM, int BN, int WGM, int WGN, int KS>
+// Only the small-block variants a shape can meet are instantiated (compile
+// time): small_block(nt) for the tile sizes that select each update shape.
+template <int BM, int BN, int WGM, int WGN, int KS, int... SBS>
 PersistKernel mk_persist(int minb, int nt) {
-    switch (small_block(nt)) {
-        case 24: return mk_persist_sb<BM, BN, WGM, WGN, KS, 24>(minb);
-        case 32: return mk_persist_sb<BM, BN, WGM, WGN, KS, 32>(minb);
-        default: return mk_persist_sb<BM, BN, WGM, WGN, KS, 0>(minb);
-    }
+    const int sb = small_block(nt);
+    PersistKernel out{};
+    auto try_one = [&](auto tag) {
+        constexpr int SB = decltype(tag)::value;
+        if (sb == SB) out = mk_persist_sb<BM, BN, WGM, WGN, KS, SB>(minb);
+    };
+    (try_one(std::integral_constant<int, SBS>{}), ...);
+    return out;  // fn == nullptr: no variant for this tile size (plan creation fails loudly)
 }
 
 // same block shapes as pick_upd, 256-thread variants (KSPLIT doubled);
 // minb = minimum resident CTAs per SM the variant is compiled for
 PersistKernel pick_persist(int nt, int minb) {
-    if (const char* f = getenv("TC_PERSIST_SHAPE")) {  // tuning override
-        if (!strcmp(f, "64")) return mk_persist<64, 64, 2, 2, 2>(minb, nt);
-        if (!strcmp(f, "32")) return mk_persist<32, 32, 2, 2, 2>(minb, nt);
-        if (!strcmp(f, "40")) return mk_persist<40, 40, 1, 1, 8>(minb, nt);
-    }
-    if (nt % 64 == 0) return mk_persist<64, 64, 2, 2, 2>(minb, nt);
-    if (nt % 80 == 0 && nt % 48 == 0) return mk_persist<80, 48, 2, 2, 2>(minb, nt);
-    if (nt % 80 == 0) return mk_persist<80, 40, 2, 1, 4>(minb, nt);
-    if (nt % 40 == 0) return mk_persist<40, 40, 1, 1, 8>(minb, nt);
-    if (nt >= 96) return mk_persist<64, 64, 2, 2, 2>(minb, nt);
-    return mk_persist<32, 32, 2, 2, 2>(minb, nt);
+    if (nt % 64 == 0) return mk_persist<64, 64, 2, 2, 2, 0, 24, 32>(minb, nt);
+    if (nt % 80 == 0 && nt % 48 == 0) return mk_persist<80, 48, 2, 2, 2, 24>(minb, nt);
+    if (nt % 80 == 0) return mk_persist<80, 40, 2, 1, 4, 0, 32>(minb, nt);
+    if (nt % 40 == 0) return mk_persist<40, 40, 1, 1, 8, 0, 24>(minb, nt);
+    if (nt >= 96) return mk_persist<64, 64, 2, 2, 2, 0, 24, 32>(minb, nt);
+    return mk_persist<32, 32, 2, 2, 2, 0>(minb, nt);
 }
 
 int prep_kernel(const void* fn, int smem) {
@@ -1176,6 +1177,7 @@ int build_persistent(tc_plan& P) {
         std::max<size_t>((size_t)pick_persist(nt, 2).smem, potrf_smem(nt, &in_smem) + xs_bytes) > two_per_sm)
         P.persist_minb = 1;  // two CTAs cannot share an SM (packed POTRF tile too large): no register cap
     const PersistKernel K = pick_persist(nt, P.persist_minb);
+    if (!K.fn) return set_err(TC_ERR_ARG, "plan: no persistent kernel variant for tile size %d", nt);
     const size_t base = std::max<size_t>({(size_t)K.smem, potrf_smem(nt, &in_smem) + xs_bytes, (size_t)4096});
     const size_t t_full = trsm_smem_bytes<kPersistTrsmRows>(nt);
     P.persist_trsm_ring = 0;
