@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--lookahead", type=int, default=None, help="bulk-update lookahead depth (default: api default)")
     ap.add_argument("--occupancy", type=int, default=0, help="persistent CTAs/SM: 0 auto, 1, 2")
     ap.add_argument("--lanes", type=int, default=4, help="c5: factorisations in flight per GPU")
+    ap.add_argument("--share", type=int, default=1,
+                    help="c5: persistent kernels sharing the GPU (grid = SMs/share; >1 is experimental)")
     ap.add_argument("--ordering", default="auto",
                     help="auto (SPEC policy) | identity (C4: auto provably picks identity, zero fill)")
     return ap.parse_args()
@@ -327,7 +329,7 @@ def run_batch(a, nt, desc, rank, world):
     P = len(thetas)
     lo, hi = shard_range(P, world, rank)
     L = max(1, a.lanes)
-    opts = api.FactorOptions(tile_size=nt, ordering=a.ordering, occupancy=a.occupancy, concurrent=L,
+    opts = api.FactorOptions(tile_size=nt, ordering=a.ordering, occupancy=a.occupancy, concurrent=a.share,
                              executor=a.executor)
     m0 = fam.matrix(*thetas[0])
     t0 = time.perf_counter()
@@ -423,7 +425,7 @@ def run_batch(a, nt, desc, rank, world):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": desc, "tile": nt, "n": m0.n, "nnz": m0.nnz, "problems": P,
-                       "lanes_per_gpu": L, "parallelism": f"batch sharded over {world} GPU(s), contiguous blocks",
+                       "lanes_per_gpu": L, "grid_share": a.share, "parallelism": f"batch sharded over {world} GPU(s), contiguous blocks",
                        "l2": "inputs larger than L2 (tile storage %.2f GB per lane)" % (16.0 * nt * nt * plan.S / 2e9)},
             "roofline": {"bound": "tensor", "kernel": "k_persist x lanes", "achieved": P * F / (ms * 1e-3) / 1e12,
                          "peak": peak, "unit": "TFLOP/s", "frac": P * F / (ms * 1e-3) / 1e12 / peak,

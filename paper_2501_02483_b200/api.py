@@ -380,9 +380,9 @@ def logdet_many(problems, opts: FactorOptions | None = None, lanes: int = 4) -> 
     only): log-determinants of independent SPD matrices, ``lanes``
     factorisations in flight on their own streams, each lane reusing one
     pinned staging buffer and one device tile storage, results handed off
-    device-side (no per-problem host sync, no factor kept alive).  Each
-    lane's persistent kernel takes 1/lanes of the SMs.  Failures are
-    aggregated into FactorizeManyError; values equal solo factorisations.
+    device-side (no per-problem host sync, no factor kept alive).  Failures
+    are aggregated into FactorizeManyError; values equal solo
+    factorisations bitwise (with the default concurrent=1).
     """
     import dataclasses
 
@@ -390,9 +390,12 @@ def logdet_many(problems, opts: FactorOptions | None = None, lanes: int = 4) -> 
     _lib.require_device()
     o = opts or FactorOptions()
     L = max(1, int(lanes))
-    if o.concurrent == 1 and L > 1:
-        o = dataclasses.replace(o, concurrent=L)
-    elif o.concurrent < 1:  # 0: every lane's kernel takes the whole GPU
+    # lanes overlap H2D, scatter and factorisation; the persistent kernels
+    # themselves take the whole GPU each (concurrent=1).  Grid sharing
+    # (concurrent=L) is opt-in: measured 1.36x batch throughput on C5 but rare
+    # mismatches (~1e-6 relative in 2-5 of 64 log-determinants) under
+    # concurrent kernels remain open
+    if o.concurrent < 1:
         o = dataclasses.replace(o, concurrent=1)
     items = [p if isinstance(p, SymmetricCsc) else p[0] for p in problems]
     P = len(items)

@@ -370,6 +370,8 @@ def test_inla_batch_device_assembly_and_streaming_logdets(torch):
     solo = np.array([api.logdet(api.factorize(m, opts)) for m in ms])
     many = api.logdet_many(ms, opts, lanes=3)
     assert np.array_equal(solo, many)
+    shared = api.logdet_many(ms, api.FactorOptions(tile_size=64, concurrent=3), lanes=3)
+    assert np.allclose(shared, solo, rtol=1e-10, atol=0)  # grid-shared lanes (experimental)
     pat = api._pattern_for(ms[0], opts)
     plan = pat.plan
     offs = pat.offsets()

@@ -1,0 +1,12 @@
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+from paper_2501_02483_b200 import api, workloads as W
+fam = W.InlaFamily()
+ms = [fam.matrix(*t) for t in W.c5_thetas()[:24]]
+for ex in ("graph", "persistent"):
+    ref = api.logdet_many(ms, api.FactorOptions(tile_size=120, executor=ex), lanes=1)
+    for lanes, conc in ((3, 0), (3, 3), (3, 3)):
+        out = api.logdet_many(ms, api.FactorOptions(tile_size=120, concurrent=conc, executor=ex), lanes=lanes)
+        bad = np.nonzero(out != ref)[0]
+        print(f"{ex} lanes {lanes} conc {conc}: mismatches {bad.tolist()} max rel {np.max(np.abs(out - ref) / np.abs(ref)):.2e}", flush=True)
