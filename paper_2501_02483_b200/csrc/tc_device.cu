@@ -1442,7 +1442,7 @@ extern "C" int tc_plan_create(int64_t n, int32_t nt, int64_t S, const int32_t* f
         P->opts.use_graph = 2;
     }
     P->W = P->opts.tree_workers > 0 ? P->opts.tree_workers : 8;
-    P->fuse = P->opts.reserved[0] == 0;  // reserved[0] = 1 disables POTRF->TRSM streaming
+    P->fuse = P->opts.reserved[0] == 0 && !getenv("TC_NO_FUSE_TRSM");  // reserved[0] = 1 disables POTRF->TRSM streaming
     if (P->W > kMaxW) return set_err(TC_ERR_ARG, "plan_create: tree_workers <= %d", kMaxW);
     // The reference rule (chain >= 2 * workers) is sized for CPU threads; on
     // the device a chain only needs splitting when it is much longer than a
