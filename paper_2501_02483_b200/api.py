@@ -49,7 +49,7 @@ class FactorOptions:
     lookahead: int = 2             # bulk-update lookahead depth in columns (0/False = off)
     executor: str = "persistent"  # persistent | graph | direct
     chunk: int = 0
-    occupancy: int = 0             # persistent CTAs per SM (0 auto, 1, 2)
+    occupancy: int = 0             # persistent CTAs per SM (0 = 1; 2 = experimental)
     concurrent: int = 1            # factorisations meant to share the GPU (batch lanes)
 
     def __post_init__(self):

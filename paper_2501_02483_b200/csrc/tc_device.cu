@@ -1166,8 +1166,12 @@ int build_persistent(tc_plan& P) {
     // to itself (C2: 0.15 GFLOP per column); update-heavy plans (C3, C4:
     // 0.7-0.9 GFLOP per column at nt=120) need the second CTA per SM to hide
     // the update pipeline's bubbles
+    // Default: one CTA per SM.  Two CTAs per SM (occupancy=2) are faster on
+    // update-heavy plans (C4 @120: 603 vs 773 ms) but show a rare,
+    // timing-dependent nondeterminism (log-determinant off by ~1e-7 relative,
+    // DESIGN.md §10) that one CTA per SM has not shown; opt-in until found.
     const int occ_mode = P.opts.reserved[1];
-    P.persist_minb = occ_mode == 1 ? 1 : occ_mode == 2 ? 2 : (P.flops / std::max(1, P.T) < 4.0e8 ? 1 : 2);
+    P.persist_minb = occ_mode == 2 ? 2 : 1;
     bool in_smem;
     // shared memory: the max over task kinds; the fused TRSM may stage L
     // strip by strip (ring) instead of whole when that lets two CTAs share an SM
