@@ -29,7 +29,8 @@ class _Sym:
         self.h = C.c_void_p(handle)
 
     def __del__(self):
-        if getattr(self, "h", None) and self.h.value:
+        # at interpreter shutdown the module globals may already be gone
+        if getattr(self, "h", None) and self.h.value and lib is not None:
             lib.tc_symbolic_destroy(self.h)
             self.h = C.c_void_p(0)
 
