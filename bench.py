@@ -452,6 +452,7 @@ def run_ours(a, name, nt, desc, rank, world):
 
     m = build_matrix(name)
     opts = api.FactorOptions(tile_size=nt, executor=a.executor, ordering=a.ordering, occupancy=a.occupancy,
+                              concurrent=a.share,  # >1: persistent grid = SMs x occupancy / share (diagnostic)
                               **({} if a.lookahead is None else {"lookahead": a.lookahead}))
     t0 = time.perf_counter()
     pat = api._pattern_for(m, opts)

@@ -1184,7 +1184,7 @@ int build_persistent(tc_plan& P) {
     if (!K.fn) return set_err(TC_ERR_ARG, "plan: no persistent kernel variant for tile size %d", nt);
     const size_t base = std::max<size_t>({(size_t)K.smem, potrf_smem(nt, &in_smem) + xs_bytes, (size_t)4096});
     const size_t t_full = trsm_smem_bytes<kPersistTrsmRows>(nt);
-    P.persist_trsm_ring = 0;
+    P.persist_trsm_ring = getenv("TC_FORCE_TRSM_RING") ? 2 : 0;  // diagnostic: ring staging at any occupancy
     P.persist_smem = std::max(base, t_full);
     if (P.persist_minb == 2 && P.persist_smem > two_per_sm) {
         // fused TRSM stages one strip at a time (1 buffer); unfused needs a ring
