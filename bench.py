@@ -1,17 +1,26 @@
 #!/usr/bin/env python
-"""bench.py — FP64 arrowhead tile Cholesky on B200 (DESIGN.md "Measurement").
+"""bench.py — FP64 arrowhead tile Cholesky on B200 (DESIGN.md §6).
 
-One *step* = one factorisation of the workload matrix from its CSC values
-resident in HBM: device scatter into tile storage + the CUDA-graph numeric
-factorisation with fused log-determinant.  ``value`` = factorizations/s over
-all ranks (each rank factorises its own replica: weak scaling, no data-path
-collective).  ``e2e`` = the same through the public API ``api.factorize`` with
-host CSC values (pinned H2D + D2H of the result inside the timed region) and,
-for N > 1, the NCCL all-gather of the per-matrix log-determinants.
+Default workload (``--workload auto``): N=1 -> C4, the largest single-GPU
+BASELINE configuration (n=1,000,000, b=2000, t=500, HBM-resident); N>1 -> C5,
+the 64-problem INLA batch sharded over the ranks (the only workload that
+shards).
 
-    python bench.py [--workload c2] [--tile 120] [--gpus N --steps K --warmup W]
-    python bench.py --impl reference ...     # reference CPU arm (oracle port)
+One *step* (single factorisations) = device scatter of the HBM-resident CSC
+values into tile storage + one persistent-kernel factorisation with fused
+log-determinant.  ``value`` = factorizations/s over all ranks.  ``e2e`` = the
+same through the public API ``api.factorize`` from HOST CSC values (H2D,
+scatter, factorisation, D2H of logdet/fail word inside the timed region).
+The N=1 line carries ``batch_c5``: the C5 batch on one GPU (first point of
+the 1->8 curve).
+
+    python bench.py [--workload auto|c1..c5] [--tile NT] [--gpus N --steps K --warmup W]
+    python bench.py --impl reference ...     # reference CPU arm (oracle port, all host cores)
     python bench.py --measure-peaks           # FP64 DMMA / DGEMM peaks -> profiles/
+
+``--gpus N`` with N>1 re-executes itself under torch.distributed.run (one rank
+per GPU, NCCL) unless already launched that way.  The reference arm never
+imports the product package: matrices and op streams come from oracle/ only.
 """
 
 from __future__ import annotations
@@ -19,6 +28,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -29,54 +39,69 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOADS = {
-    "c1": ("arrowhead n=10,000 b=200 t=50 (BASELINE config 1)", 120),
-    "c2": ("variable-band arrowhead n=100,000 max band 1,000 t=200 (BASELINE config 2)", 120),
-    "c3": ("INLA 2000x100+10 (n=200,010) kappa=.5 rho=.9 tau=1e-3 (BASELINE config 3)", 240),
-    "c4": ("arrowhead n=1,000,000 b=2000 t=500 (BASELINE config 4)", 240),
-    "c5": ("batch of 64 INLA factorizations (C3 pattern, theta on a 4x4x4 grid) (BASELINE config 5)", 120),
-}
+# default tile per workload (C3/C5: BASELINE's stated 240 is slower than 120
+# on this executor, see profiles/; tile size is swept with --tile)
+DEFAULT_NT = {"c1": 120, "c2": 120, "c3": 120, "c4": 120, "c5": 120}
+N_OF = {"c1": 10_000, "c2": 100_000, "c3": 200_010, "c4": 1_000_000, "c5": 200_010}
 PEAKS_FILE = os.path.join(ROOT, "profiles", "fp64_peaks.json")
 FP64_FALLBACK_TFLOPS = 37.0  # NVIDIA B200 FP64 (tensor) nominal, used only if unmeasured
+CPU_SAMPLE_FLOPS_OURS = 4.0e11   # ~15 s of one core (cpu_baseline leg)
+CPU_SAMPLE_FLOPS_REF = 1.0e11    # ~4 s per process per step (reference arm)
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="auto", choices=["auto", "c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-batch", action="store_true", help="N=1: skip the batch_c5 sub-measurement")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--measure-peaks", action="store_true")
     ap.add_argument("--ref-procs", type=int, default=0)
     ap.add_argument("--executor", default="persistent", choices=["persistent", "graph", "direct"])
     ap.add_argument("--lookahead", type=int, default=None, help="bulk-update lookahead depth (default: api default)")
-    ap.add_argument("--occupancy", type=int, default=0, help="persistent CTAs/SM: 0 auto, 1, 2")
     ap.add_argument("--lanes", type=int, default=4, help="c5: factorisations in flight per GPU")
-    ap.add_argument("--share", type=int, default=1,
-                    help="c5: persistent kernels sharing the GPU (grid = SMs/share; >1 is experimental)")
     ap.add_argument("--ordering", default="auto",
                     help="auto (SPEC policy) | identity (C4: auto provably picks identity, zero fill)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
-def build_matrix(name):
-    from paper_2501_02483_b200 import workloads as W
+def workload_of(a) -> str:
+    if a.workload != "auto":
+        return a.workload
+    return "c4" if a.gpus <= 1 else "c5"
+
+
+def maybe_spawn(a) -> bool:
+    """--gpus N>1 outside torchrun: re-exec under torch.distributed.run."""
+    if a.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def common_config(name, nt, world, a):
+    """The workload description both arms print (identical by construction)."""
+    from oracle.workloads import WORKLOAD_DESC
+    cfg = {"workload": WORKLOAD_DESC[name], "tile": nt, "n": N_OF[name], "ordering": a.ordering,
+           "l2": "inputs larger than L2 (tile storage >= 0.9 GB per factorisation; 126 MB L2)"}
     if name == "c5":
-        return W.c3()
-    if name == "c1":
-        return W.c1()
-    if name == "c2":
-        return W.c2_variable_band()
-    if name == "c3":
-        return W.c3()
-    if name == "c4":
-        return W.c4()
-    raise ValueError(name)
+        cfg["problems"] = 64
+        cfg["parallelism"] = f"batch sharded over {world} GPU(s), contiguous blocks, NCCL all-gather of results"
+    else:
+        cfg["parallelism"] = f"replicas x{world} (one factorisation per GPU per step)"
+    return cfg
 
 
 # ------------------------------------------------------------------ clocks --
@@ -95,10 +120,11 @@ class Clocks:
     def start(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200",
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
                  "-i", str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            time.sleep(0.3)  # sampler running before the timed region starts
         except OSError:
             self.proc = None
 
@@ -109,6 +135,7 @@ class Clocks:
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -203,49 +230,70 @@ def hbm_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-# -------------------------------------------------------- CPU (oracle) arm --
-def _oracle_setup(m, nt):
-    import oracle as O
-    from paper_2501_02483_b200 import ctsf, symbolic
-    g = ctsf.build_tile_grid(m, nt)
-    s = symbolic.tile_symbolic_factorize(g)
-    fg = s.factor_grid
-    ts = symbolic.enumerate_tasks(s)
-    tasks = {"type": ts.task_type, "m": ts.m, "k": ts.k, "n": ts.n, "target": ts.target}
-    op, dst, s1, s2, _ = O.compile_ops(tasks, fg.slot_map, fg.n_tiles)
-    tpl = ctsf.pack_into_grid(m, fg).storage
-    return op, dst, s1, s2, tpl
+# ----------------------------------------------- CPU arms (oracle only) --
+def oracle_sample(name, nt, target_flops, with_storage=True):
+    """Bounded sample of one factorisation of workload `name` for the CPU
+    arms: the reference op stream of the first K tile columns (oracle/
+    workloads.prefix_problem), K chosen for ~target_flops tile flops; plus the
+    tile flops of the WHOLE factorisation, so sample time scales to
+    factorizations/s exactly by flop fraction."""
+    import oracle.workloads as OW
+    if name == "c4":
+        n, b, t = OW.C4_SPEC
+        F, _ = OW.arrowhead_tile_flops(n, b, t, nt)
+        T = -(-n // nt)
+        K = max(1, min(T, int(np.ceil(target_flops / (F / T)))))
+        nn, cp, ri, v = OW.c4_columns(min(K * nt, n - t))
+        pr = OW.prefix_problem(nn, cp, ri, v, nt, K, with_storage=with_storage)
+        pr["F_total"] = F
+        return pr
+    gen = {"c1": OW.c1, "c2": OW.c2, "c3": OW.c3, "c5": OW.c3}[name]
+    n, cp, ri, v = gen()
+    full = OW.prefix_problem(n, cp, ri, v, nt, 1 << 30, with_storage=False)
+    T = full["columns"]
+    F = full["flops"]
+    if F <= target_flops * 1.2:
+        pr = OW.prefix_problem(n, cp, ri, v, nt, T, with_storage=with_storage)
+    else:
+        # prefix flops are not uniform per column: grow K geometrically
+        K = max(1, int(T * target_flops / F))
+        while True:
+            pr = OW.prefix_problem(n, cp, ri, v, nt, K, with_storage=False)
+            if pr["flops"] >= target_flops or K >= T:
+                break
+            K = min(T, int(K * 1.25) + 1)
+        pr = OW.prefix_problem(n, cp, ri, v, nt, K, with_storage=with_storage)
+    pr["F_total"] = F
+    return pr
 
 
-def cpu_baseline(m, nt):
-    """Oracle port of the reference run_ops (numba loops + OpenBLAS dgemm via
-    np.dot, 1 thread) on the full workload factorisation."""
+def time_sample(pr):
+    """Oracle run_ops (numba loops + OpenBLAS via np.dot, 1 thread) over the
+    sample; returns (seconds, factor storage)."""
     import oracle as O
-    op, dst, s1, s2, tpl = _oracle_setup(m, nt)
+    nt = pr["storage"].shape[1]
     sc = np.zeros((0, nt, nt))
-    warm = tpl[:2].copy()
-    O.run_ops(warm, sc, op[:0], dst[:0], s1[:0], s2[:0], 0, 0)  # JIT
-    small = np.zeros((3, nt, nt))
-    for i in range(3):
-        small[i] = np.eye(nt) * 4.0
-    O.potrf_t(small[0].T.copy())
-    st = tpl.copy()
+    O.run_ops(pr["storage"][:1].copy(), sc, pr["op"][:0], pr["dst"][:0], pr["src1"][:0], pr["src2"][:0], 0, 0)
+    st = pr["storage"].copy()
     t0 = time.perf_counter()
-    p, info = O.run_ops(st, sc, op, dst, s1, s2, 0, op.size)
+    p, info = O.run_ops(st, sc, pr["op"], pr["dst"], pr["src1"], pr["src2"], 0, pr["ops"])
     dt = time.perf_counter() - t0
-    assert info == -1
-    return dt
+    if info != -1:
+        raise RuntimeError(f"oracle sample failed at op {p} (info {info})")
+    return dt, st
 
 
 def _ref_worker(args):
-    name, nt, steps, q_in, q_out = args
+    path, q_in, q_out = args
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     import oracle as O
-    m = build_matrix(name)
-    op, dst, s1, s2, tpl = _oracle_setup(m, nt)
+    z = np.load(path)
+    tpl = z["storage"]
+    op, dst, s1, s2 = z["op"], z["dst"], z["src1"], z["src2"]
+    nt = tpl.shape[1]
     sc = np.zeros((0, nt, nt))
     st = np.empty_like(tpl)
-    O.run_ops(st[:0], sc, op[:0], dst[:0], s1[:0], s2[:0], 0, 0)
+    O.run_ops(tpl[:1].copy(), sc, op[:0], dst[:0], s1[:0], s2[:0], 0, 0)  # JIT
     q_out.put("ready")
     while True:
         cmd = q_in.get()
@@ -253,30 +301,36 @@ def _ref_worker(args):
             break
         np.copyto(st, tpl)
         t0 = time.perf_counter()
-        O.run_ops(st, sc, op, dst, s1, s2, 0, op.size)
-        q_out.put(time.perf_counter() - t0)
+        p, info = O.run_ops(st, sc, op, dst, s1, s2, 0, op.size)
+        q_out.put((time.perf_counter() - t0, int(info)))
 
 
-def run_reference(a, name, nt, desc):
-    """Reference CPU implementation (oracle port of _backend_numba.run_ops) on
-    the box's host cores: one factorisation per process per step
-    (Appendix-A batch semantics; threads scale poorly, survey §8(d))."""
+def run_reference(a, name, nt, world):
+    """Reference CPU implementation of the path (oracle port of
+    _backend_numba.run_ops over the reference op stream) on
+    the box's host cores: one process per core, each running the same
+    bounded sample (the first K tile columns of one factorisation) per step;
+    value = processes x (sample tile flops / factorisation tile flops) / wall."""
     import multiprocessing as mp
+    import tempfile
     cores = len(os.sched_getaffinity(0))
-    m = build_matrix(name)
-    est = (m.nnz * 12 + 3 * 8 * nt * nt * (m.nnz // max(1, nt)) // max(1, nt)) / 1e9
+    t0 = time.perf_counter()
+    pr = oracle_sample(name, nt, CPU_SAMPLE_FLOPS_REF)
+    setup_s = time.perf_counter() - t0
+    per_proc = 2.5 * pr["storage"].nbytes / 1e9 + 0.5
     try:
         import psutil
         mem = psutil.virtual_memory().available / 1e9
     except ImportError:
-        mem = 64.0
-    per_proc = max(2.0, 2.5 * est)
+        mem = 32.0
     procs = a.ref_procs or max(1, min(cores, int(mem * 0.6 / per_proc)))
-    del m
+    tmpd = tempfile.mkdtemp(prefix="tc_ref_")
+    path = os.path.join(tmpd, "sample.npz")
+    np.savez(path, storage=pr["storage"], op=pr["op"], dst=pr["dst"], src1=pr["src1"], src2=pr["src2"])
     ctx = mp.get_context("spawn")
     qin = [ctx.Queue() for _ in range(procs)]
     qout = ctx.Queue()
-    ps = [ctx.Process(target=_ref_worker, args=((name, nt, 0, qin[i], qout),)) for i in range(procs)]
+    ps = [ctx.Process(target=_ref_worker, args=((path, qin[i], qout),)) for i in range(procs)]
     for p in ps:
         p.start()
     for _ in ps:
@@ -286,8 +340,8 @@ def run_reference(a, name, nt, desc):
         t0 = time.perf_counter()
         for q in qin:
             q.put(1)
-        for _ in ps:
-            qout.get()
+        res = [qout.get() for _ in ps]
+        assert all(r[1] == -1 for r in res), "reference sample failed"
         return time.perf_counter() - t0
 
     for _ in range(a.warmup):
@@ -297,29 +351,38 @@ def run_reference(a, name, nt, desc):
         q.put(None)
     for p in ps:
         p.join()
+    try:
+        os.remove(path)
+        os.rmdir(tmpd)
+    except OSError:
+        pass
     wall = float(np.mean(walls))
-    value = procs / wall
-    line = {"impl": "reference", "metric": "factorizations/s (FP64 time-to-factor)", "value": value,
-            "unit": "factorizations/s", "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": wall * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": desc, "tile": nt, "processes": procs},
-            "cpu_baseline": {"value": value, "unit": "factorizations/s", "cores": procs, "kind": "port",
-                             "sample": f"{procs} concurrent full factorisations per step (one per process, "
-                                       f"oracle run_ops = numba loops + OpenBLAS dgemm, 1 thread each)"},
-            "e2e": {"value": value, "unit": "factorizations/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+    frac = pr["flops"] / pr["F_total"]
+    value = procs * frac / wall
+    metric, unit = ("batched factorizations/s (FP64, C5)" if name == "c5" else
+                    "factorizations/s (FP64 time-to-factor)"), "factorizations/s"
+    sample = (f"{procs} processes x the first {pr['columns']} tile columns of one {name} factorisation "
+              f"({pr['ops']} reference ops, {pr['flops']:.3e} of {pr['F_total']:.3e} tile flops = "
+              f"{100 * frac:.2f}%) per step; oracle run_ops = numba loops + OpenBLAS dgemm, 1 thread each")
+    line = {"impl": "reference", "metric": metric, "value": value, "unit": unit, "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": wall * 1e3,
+            "higher_is_better": True, "scaling": "strong" if name == "c5" else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": common_config(name, nt, world, a),
+            "cpu_baseline": {"value": value, "unit": unit, "cores": procs, "kind": "port", "sample": sample,
+                             "wall_s_per_step": wall, "sample_fraction": frac, "setup_s": setup_s},
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------- GPU arm, batch --
-def run_batch(a, nt, desc, rank, world):
+def run_batch(a, nt, rank, world, sub=False):
     """C5: 64 INLA factorisations Q(theta) sharing the C3 pattern, sharded in
     contiguous blocks over the ranks (strong scaling), `lanes` in flight per
     GPU.  Device step: values assembled on the GPU from the 13 basis vectors
     of the family (tc_plan_pack_lincomb), factorised, log-determinants handed
-    off device-side.  e2e: api.logdet_many_sharded from host CSC values (H2D
-    per problem) + one NCCL all-gather of the 64 log-determinants."""
+    off device-side, one NCCL all-gather of the 64 log-determinants (N>1).
+    e2e: api.logdet_many_sharded from host CSC values (H2D per problem) + the
+    all-gather."""
     import torch
     import torch.distributed as dist
     from paper_2501_02483_b200 import api, matcore, workloads as W
@@ -329,8 +392,7 @@ def run_batch(a, nt, desc, rank, world):
     P = len(thetas)
     lo, hi = shard_range(P, world, rank)
     L = max(1, a.lanes)
-    opts = api.FactorOptions(tile_size=nt, ordering=a.ordering, occupancy=a.occupancy, concurrent=a.share,
-                             executor=a.executor)
+    opts = api.FactorOptions(tile_size=nt, ordering=a.ordering, executor=a.executor)
     m0 = fam.matrix(*thetas[0])
     t0 = time.perf_counter()
     pat = api._pattern_for(m0, opts)
@@ -347,13 +409,16 @@ def run_batch(a, nt, desc, rank, world):
     nloc = hi - lo
     fail = torch.zeros(max(1, nloc), dtype=torch.int64, device="cuda")
     ld = torch.zeros(max(1, nloc), dtype=torch.float64, device="cuda")
+    cap = -(-P // world)
+    gbuf = torch.zeros(cap, dtype=torch.float64, device="cuda")
+    gout = [torch.zeros(cap, dtype=torch.float64, device="cuda") for _ in range(world)]
+    main = torch.cuda.current_stream()
 
     def step():
         start = torch.cuda.Event(enable_timing=True)
-        start.record()
-        ends = []
+        start.record(main)
         for s in streams:
-            s.wait_event(start)
+            s.wait_stream(main)
         for j in range(nloc):
             lane = j % L
             s = streams[lane]
@@ -362,13 +427,16 @@ def run_batch(a, nt, desc, rank, world):
             plan.factorize_async(stor[lane], lane, sh)
             plan.copy_result(lane, sh, fail[j:j + 1], ld[j:j + 1])
         for s in streams:
-            e = torch.cuda.Event(enable_timing=True)
-            e.record(s)
-            ends.append(e)
-        return start, ends
+            main.wait_stream(s)
+        gbuf[:nloc].copy_(ld[:nloc])
+        if world > 1:
+            dist.all_gather(gout, gbuf)
+        end = torch.cuda.Event(enable_timing=True)
+        end.record(main)
+        return start, end
 
     t0 = time.perf_counter()
-    for _ in range(max(a.warmup, 1)):
+    for _ in range(max(a.warmup if not sub else 1, 1)):
         step()
     torch.cuda.synchronize()
     print(f"[c5] warm-up {time.perf_counter() - t0:.1f} s", file=sys.stderr, flush=True)
@@ -376,18 +444,16 @@ def run_batch(a, nt, desc, rank, world):
     if not ok:
         raise RuntimeError("a batch factorisation failed")
     ld_ref = ld[:nloc].clone()
+    steps = 1 if sub else a.steps
     if world > 1:
         dist.barrier()
     clk = Clocks(int(os.environ.get("LOCAL_RANK", "0")))
     clk.start()
     torch.cuda.synchronize()
-    evs = [step() for _ in range(a.steps)]
+    evs = [step() for _ in range(steps)]
     torch.cuda.synchronize()
     clocks = clk.stop()
-    print(f"[c5] timed steps done", file=sys.stderr, flush=True)
-    ms = evs[0][0].elapsed_time(evs[-1][0]) if a.steps > 1 else 0.0
-    ms = max(evs[-1][0].elapsed_time(e) for e in evs[-1][1]) + ms
-    ms /= a.steps
+    ms = evs[0][0].elapsed_time(evs[-1][1]) / steps
     repro_dev = bool(torch.equal(ld[:nloc], ld_ref))
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -399,7 +465,7 @@ def run_batch(a, nt, desc, rank, world):
         probs[i] = fam.matrix(*thetas[i])
     h2d = sum(probs[i].nnz * 8 for i in range(lo, hi))
     e2e_ms = []
-    for i in range(a.e2e_steps + 1):
+    for i in range((1 if sub else a.e2e_steps) + 1):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -415,45 +481,68 @@ def run_batch(a, nt, desc, rank, world):
         e2e = float(t.item())
     ldr = ld_ref.cpu().numpy()[:nloc]
     repro_api = bool(np.array_equal(lds[lo:hi], ldr))
-    max_rel = float(np.max(np.abs(lds[lo:hi] - ldr) / np.abs(ldr))) if nloc else 0.0
-    if not repro_api:
-        bad = np.nonzero(lds[lo:hi] != ldr)[0]
-        print(f"[c5] mismatch at {bad.tolist()[:16]}: {(lds[lo:hi] - ldr)[bad][:8]}", file=sys.stderr, flush=True)
     peak, peak_src = fp64_peak()
     value = P * 1000.0 / ms
     line = {"metric": "batched factorizations/s (FP64, C5)", "value": value, "unit": "factorizations/s",
-            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+            "n_gpus": world, "steps": steps, "warmup": a.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": desc, "tile": nt, "n": m0.n, "nnz": m0.nnz, "problems": P,
-                       "lanes_per_gpu": L, "grid_share": a.share, "parallelism": f"batch sharded over {world} GPU(s), contiguous blocks",
-                       "l2": "inputs larger than L2 (tile storage %.2f GB per lane)" % (16.0 * nt * nt * plan.S / 2e9)},
+            "data": "synthetic", "config": common_config("c5", nt, world, a),
+            "lanes_per_gpu": L, "nnz": m0.nnz,
             "roofline": {"bound": "tensor", "kernel": "k_persist x lanes", "achieved": P * F / (ms * 1e-3) / 1e12,
                          "peak": peak, "unit": "TFLOP/s", "frac": P * F / (ms * 1e-3) / 1e12 / peak,
                          "traffic": None, "peak_source": peak_src},
-            "gpu_launches": 3 * max(1, nloc), "setup_s": setup_s,
-            "bitwise_reproducible": repro_dev and repro_api, "logdet_max_rel_diff": max_rel,
+            "gpu_launches": 5 * max(1, nloc) * steps, "setup_s": setup_s,
+            "bitwise_reproducible": repro_dev and repro_api,
             "e2e": {"value": P * 1000.0 / e2e, "unit": "factorizations/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(16 * nloc + 8 * P), "ms_per_step": e2e,
                     "path": "api.logdet_many_sharded(host CSC values)" + (" + NCCL all_gather" if world > 1 else "")},
             "clocks": clocks}
+    if sub:
+        return {k: line[k] for k in ("metric", "value", "unit", "ms_per_step", "steps", "roofline", "e2e",
+                                     "bitwise_reproducible", "lanes_per_gpu", "clocks")}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
 
 # --------------------------------------------------------------- GPU arm --
-def run_ours(a, name, nt, desc, rank, world):
+def build_matrix(name):
+    from paper_2501_02483_b200 import workloads as W
+    return {"c1": W.c1, "c2": W.c2_variable_band, "c3": W.c3, "c4": W.c4}[name]()
+
+
+def prefix_parity(pat, storage, pr, nt):
+    """Compare the device factor with the oracle's factor of the first K tile
+    columns (the CPU sample): relative Frobenius difference over those tiles
+    and the partial log-determinant (2 sum log diag over columns < K)."""
+    fg = pat.symbolic.factor_grid
+    K = pr["columns"]
+    sel = np.nonzero(pr["gcol"] < K)[0]
+    slots = fg.slots_of(pr["grow"][sel], pr["gcol"][sel])
+    assert (slots >= 0).all()
+    import torch
+    got = storage[torch.from_numpy(slots).to(storage.device)].cpu().numpy()
+    ref = pr["factor"][sel]
+    rel = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+    dg = np.nonzero(pr["grow"][sel] == pr["gcol"][sel])[0]
+    ld_g = 2.0 * sum(float(np.sum(np.log(np.diagonal(got[i].T)))) for i in dg)
+    ld_r = 2.0 * sum(float(np.sum(np.log(np.diagonal(ref[i].T)))) for i in dg)
+    return {"prefix_columns": int(K), "prefix_tiles": int(sel.size), "factor_rel_diff": rel,
+            "partial_logdet_rel_diff": abs(ld_g - ld_r) / abs(ld_r)}
+
+
+def run_ours(a, name, nt, rank, world):
     if name == "c5":
-        return run_batch(a, nt, desc, rank, world)
+        return run_batch(a, nt, rank, world)
     import torch
     import torch.distributed as dist
     from paper_2501_02483_b200 import api
     from paper_2501_02483_b200._lib import check, lib, f64p, i64p
 
+    t0 = time.perf_counter()
     m = build_matrix(name)
-    opts = api.FactorOptions(tile_size=nt, executor=a.executor, ordering=a.ordering, occupancy=a.occupancy,
-                              concurrent=a.share,  # >1: persistent grid = SMs x occupancy / share (diagnostic)
-                              **({} if a.lookahead is None else {"lookahead": a.lookahead}))
+    gen_s = time.perf_counter() - t0
+    opts = api.FactorOptions(tile_size=nt, executor=a.executor, ordering=a.ordering,
+                             **({} if a.lookahead is None else {"lookahead": a.lookahead}))
     t0 = time.perf_counter()
     pat = api._pattern_for(m, opts)
     setup_s = time.perf_counter() - t0
@@ -497,14 +586,40 @@ def run_ours(a, name, nt, desc, rank, world):
     fail, ld2 = plan.collect(0, sh)
     if fail >= 0:
         raise RuntimeError(f"timed factorisation failed at {fail}")
-    # bitwise reproducibility of the timed steps vs the warm-up (reported, not
-    # fatal: DESIGN.md §10 lists a rare nondeterminism still under investigation)
     reproducible = bool(ld2 == ld)
     if not reproducible:
         print(f"[bench] timed logdet differs from warm-up: {ld2!r} vs {ld!r}", file=sys.stderr, flush=True)
 
+    # ---- dominant kernel: k_persist alone, CUDA events on its stream
+    peak, peak_src = fp64_peak()
+    hbm, hbm_src = hbm_peak()
+    kms = []
+    for _ in range(max(2, min(a.steps, 5))):
+        plan.pack(vals_dev, offs, storage, sh)
+        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        k0.record(stream)
+        plan.factorize_async(storage, 0, sh)
+        k1.record(stream)
+        torch.cuda.synchronize()
+        kms.append(k0.elapsed_time(k1))
+    kernel_ms = float(np.mean(kms))
+
+    # ---- parity at full size: device backward error + oracle prefix factor
+    parity = None
+    pr = None
+    if rank == 0 and world == 1 and not (a.no_parity and a.no_cpu_baseline):
+        pr = oracle_sample(name, nt, CPU_SAMPLE_FLOPS_OURS)
+        cpu_dt, pr["factor"] = time_sample(pr)
+    if rank == 0 and not a.no_parity:
+        parity = {}
+        if pr is not None:
+            parity.update(prefix_parity(pat, storage, pr, nt))
+        parity.update(device_backward_error(pat, m, storage, vals_dev, offs, sh))
+        parity["tolerances"] = {"backward_error": 1e-12, "factor_rel_diff": 1e-12, "logdet_rel_diff": 1e-10}
+
     # ---- end to end through the public API (host values, H2D/D2H inside)
     e2e_ms = []
+    del_vals = vals_dev
     for i in range(a.e2e_steps + 1):
         torch.cuda.synchronize()
         if world > 1:
@@ -527,28 +642,13 @@ def run_ours(a, name, nt, desc, rank, world):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = float(t.item())
 
-    # ---- dominant kernel: the factorisation kernel alone (persistent executor:
-    # one k_persist launch per step), CUDA events on its stream, scatter excluded
-    peak, peak_src = fp64_peak()
-    hbm, hbm_src = hbm_peak()
-    kms = []
-    for _ in range(max(2, min(a.steps, 5))):
-        plan.pack(vals_dev, offs, storage, sh)
-        k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        k0.record(stream)
-        plan.factorize_async(storage, 0, sh)
-        k1.record(stream)
-        torch.cuda.synchronize()
-        kms.append(k0.elapsed_time(k1))
-    kernel_ms = float(np.mean(kms))
-    # diagnostic: serialised per-class breakdown (direct launches of the same plan)
     prof = None
-    if not a.no_profile and rank == 0:
+    if not a.no_profile and rank == 0 and name != "c4":
         nc = 7
         pms = np.zeros(nc)
         pcnt = np.zeros(nc, dtype=np.int64)
         pfl = np.zeros(nc)
-        plan.pack(vals_dev, offs, storage, sh)
+        plan.pack(del_vals, offs, storage, sh)
         check("tc_plan_profile", lib.tc_plan_profile(plan.h, storage.data_ptr(), sh, nc,
                                                      pms.ctypes.data_as(f64p), pcnt.ctypes.data_as(i64p),
                                                      pfl.ctypes.data_as(f64p)))
@@ -562,14 +662,13 @@ def run_ours(a, name, nt, desc, rank, world):
     value = world * 1000.0 / ms
     kname = {"persistent": "k_persist (persistent dataflow executor)", "graph": "CUDA graph of k_update/k_potrf/k_trsm",
              "direct": "direct k_update/k_potrf/k_trsm launches"}[a.executor]
+    per_step = 4 if a.executor == "persistent" else int(info["launches"]) + 3
     line = {"metric": "factorizations/s (FP64 time-to-factor)", "value": value, "unit": "factorizations/s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": desc, "tile": nt, "n": m.n, "nnz": m.nnz, "tiles_per_side": T, "slots": S,
-                       "ordering": a.ordering, "executor": a.executor, "occupancy": a.occupancy, "lookahead": opts.lookahead,
-                       "parallelism": f"replicas x{world} (one factorisation per GPU per step)",
-                       "l2": "inputs larger than L2 (tile storage %.2f GB)" % (B / 2 / 1e9)},
+            "data": "synthetic", "config": common_config(name, nt, world, a),
+            "structure": {"nnz": m.nnz, "tiles_per_side": T, "slots": S, "tile_storage_gb": B / 2 / 1e9,
+                          "executor": a.executor, "lookahead": opts.lookahead},
             "time_to_factor_ms": ms, "gflops_tile": F / (ms * 1e-3) / 1e9,
             "gflops_useful": useful / (ms * 1e-3) / 1e9 if useful else None,
             "fp64_roofline": {"time_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms, "tile_flops": F,
@@ -581,9 +680,11 @@ def run_ours(a, name, nt, desc, rank, world):
                          "kernel_ms": kernel_ms, "peak_source": peak_src,
                          "note": "algorithmic tile flops (SYRK = nt^3, GEMM = 2 nt^3, POTRF = nt^3/3, TRSM = nt^3) "
                                  "per launch / CUDA-event launch time; traffic: see profiles/"},
-            "gpu_launches": (1 if a.executor == "persistent" else int(info["launches"])) + 2,
-            "setup_s": setup_s, "logdet": ld, "bitwise_reproducible": reproducible,
-            "logdet_rel_diff": abs(ld2 - ld) / abs(ld) if ld else 0.0}
+            "gpu_launches": per_step * a.steps, "gpu_launches_per_step": per_step,
+            "setup_s": setup_s, "generate_s": gen_s, "pattern_times_s": pat.times,
+            "logdet": ld, "bitwise_reproducible": reproducible}
+    if parity is not None:
+        line["parity"] = parity
     if prof:
         line["profile_direct"] = prof
     line["e2e"] = {"value": world * 1000.0 / e2e, "unit": "factorizations/s",
@@ -591,13 +692,44 @@ def run_ours(a, name, nt, desc, rank, world):
                    "ms_per_step": e2e, "path": "api.factorize(SymmetricCsc host values) + logdet"
                    + (" + NCCL all_gather of logdets" if world > 1 else "")}
     line["clocks"] = clocks
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        dt = cpu_baseline(m, nt)
-        line["cpu_baseline"] = {"value": 1.0 / dt, "unit": "factorizations/s", "cores": 1, "kind": "port",
-                                "sample": f"one full {name} factorisation (oracle run_ops, numba + OpenBLAS "
-                                          f"dgemm, OPENBLAS_NUM_THREADS=1), {dt:.2f} s"}
+    if rank == 0 and world == 1 and not a.no_cpu_baseline and pr is not None:
+        frac = pr["flops"] / pr["F_total"]
+        line["cpu_baseline"] = {"value": frac / cpu_dt, "unit": "factorizations/s", "cores": 1, "kind": "port",
+                                "sample": f"first {pr['columns']} tile columns of one {name} factorisation "
+                                          f"({pr['ops']} reference ops, {pr['flops']:.3e} of {pr['F_total']:.3e} "
+                                          f"tile flops = {100 * frac:.2f}%) in {cpu_dt:.2f} s; oracle run_ops "
+                                          f"(numba + OpenBLAS dgemm, OPENBLAS_NUM_THREADS=1), scaled by flop fraction"}
+    del m, vals_dev, del_vals, storage
+    if world == 1 and not a.no_batch and name == "c4":
+        import gc
+        gc.collect()
+        api.clear_plan_cache()
+        torch.cuda.empty_cache()
+        line["batch_c5"] = run_batch(a, DEFAULT_NT["c5"], rank, world, sub=True)
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def device_backward_error(pat, m, storage, vals_dev, offs, sh):
+    """||PAP^T - LL^T||_F / ||A||_F by the device replay of the reference op
+    stream (tc_replay_residual, reference _backend_numba.py:136-185) against
+    the packed original."""
+    from paper_2501_02483_b200 import symbolic
+    from paper_2501_02483_b200.backend import impl
+    import torch
+    op, dst, s1, s2, _ = symbolic.compile_ops(pat.symbolic)
+    tpl = pat.plan.new_storage()
+    pat.plan.pack(vals_dev, offs, tpl, sh)
+    fg = pat.symbolic.factor_grid
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2 = impl.replay_residual(storage, tpl, op, dst, s1, s2, fg.tile_rows == fg.tile_cols)
+    dt = time.perf_counter() - t0
+    del tpl
+    v = m.values
+    d = v[m.col_ptr[:-1]]
+    anorm = float(np.sqrt(2.0 * np.dot(v, v) - np.dot(d, d)))
+    return {"backward_error": float(np.sqrt(e2)) / anorm, "replay_s": dt}
 
 
 def _useful_flops(pat):
@@ -616,14 +748,14 @@ def main():
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    name = a.workload
-    desc, default_nt = WORKLOADS[name]
-    nt = a.tile or default_nt
+    name = workload_of(a)
+    nt = a.tile or DEFAULT_NT[name]
     if a.impl == "reference":
         if rank != 0:
             return
-        run_reference(a, name, nt, desc)
+        run_reference(a, name, nt, max(world, a.gpus))
         return
+    maybe_spawn(a)
     import torch
     if world > 1:
         import torch.distributed as dist
@@ -634,7 +766,7 @@ def main():
             measure_peaks()
         return
     try:
-        run_ours(a, name, nt, desc, rank, world)
+        run_ours(a, name, nt, rank, world)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -12,6 +12,7 @@ plan and scatter map (the INLA batch case).
 from __future__ import annotations
 
 import hashlib
+import os
 import time
 from collections import OrderedDict
 from dataclasses import dataclass, field
@@ -34,13 +35,27 @@ _ORDERINGS = ("auto", "identity", "partial-rcm", "min-degree", "adaptable-nd")
 _REDUCTIONS = ("auto", "on", "off")
 
 
+def _experimental_enabled() -> bool:
+    return os.environ.get("TILECHOL_EXPERIMENTAL", "") not in ("", "0")
+
+
 @dataclass(frozen=True)
 class FactorOptions:
     """SPEC.md:482-485 options plus B200 plan knobs.
 
-    ``workers`` keeps its reference meaning for the tree-reduction rule
-    (chains >= 2*workers are split); with workers < 2 the device default of 8
-    partial accumulators is used."""
+    ``tree_reduction``: "off" never splits a chain; "on" is the
+    reference rule, chains with accum >= 2*workers are split over ``workers``
+    partial tiles (reference symbolic.py:218-269); "auto" is the device rule:
+    W = ``workers`` (8 when workers < 2) partials, split only chains with
+    accum >= 8*W (on the GPU only the ~T-long arrow x arrow chains benefit;
+    the reference's 2*workers threshold is sized for CPU threads).  The split
+    changes the summation order, so "on"/"auto" factors agree with the
+    sequential reference within rounding, not bitwise.
+
+    ``occupancy`` = 2 (two persistent CTAs per SM) and ``concurrent`` > 1
+    (grid-shared batch lanes) are experimental: they have shown rare
+    log-determinant drift and are rejected unless the
+    environment sets TILECHOL_EXPERIMENTAL=1."""
 
     tile_size: int = 120
     workers: int = 1
@@ -63,6 +78,13 @@ class FactorOptions:
             raise ValueError(f"unknown tree_reduction policy {self.tree_reduction!r}")
         if self.executor not in ("persistent", "graph", "direct"):
             raise ValueError(f"unknown executor {self.executor!r}")
+        if self.occupancy not in (0, 1, 2):
+            raise ValueError(f"occupancy must be 0, 1 or 2, got {self.occupancy}")
+        if self.concurrent < 1:
+            raise ValueError(f"concurrent must be >= 1, got {self.concurrent}")
+        if (self.occupancy == 2 or self.concurrent > 1) and not _experimental_enabled():
+            raise ValueError("occupancy=2 / concurrent>1 are experimental (rare log-determinant drift, "
+                             "DESIGN.md §10); set TILECHOL_EXPERIMENTAL=1 to enable them")
 
     def plan_options(self) -> PlanOptions:
         W = self.workers if self.workers >= 2 else 8
@@ -138,9 +160,13 @@ _MAX_CACHE = 8
 
 
 def clear_plan_cache() -> None:
+    """Drop cached plans/patterns and unregister every page-locked caller array."""
     _PLANS.clear()
     _PATTERNS.clear()
     _SAME_ARRAYS.clear()
+    while _REGISTERED:
+        (p, _), _a = _REGISTERED.popitem(last=False)
+        _lib.lib.tc_host_unregister(_lib.C.c_void_p(p))
 
 
 def _lru(cache, key, make):
@@ -194,7 +220,7 @@ def _choose_ordering(m: SymmetricCsc, opts: FactorOptions, stats) -> Permutation
         return min_degree(m)
     if pol == "adaptable-nd":
         return adaptable_nd(m, stats)
-    return select_ordering(m, [rcm(m, pinned_tail=stats.thickness), adaptable_nd(m, stats)])
+    return select_ordering(m, [lambda: rcm(m, pinned_tail=stats.thickness), lambda: adaptable_nd(m, stats)])
 
 
 # ------------------------------------------------------------- factorize --
@@ -203,20 +229,30 @@ def _stream_handle(stream) -> int:
 
 
 # host arrays page-locked in place (cudaHostRegister), most recent last; the
-# entries hold a reference so the memory stays valid while registered
+# entries hold a reference so the memory stays valid while registered.  At
+# most _REGISTERED_MAX arrays / _REGISTERED_CAP bytes stay pinned (LRU);
+# clear_plan_cache() releases all of them.
 _REGISTERED: "OrderedDict[tuple, np.ndarray]" = OrderedDict()
-_REGISTERED_CAP = 16 << 30
+_REGISTERED_CAP = 32 << 30
+_REGISTERED_MAX = 2
 
 
 def _registered(vals: np.ndarray) -> bool:
-    """Page-lock a caller-owned values array once (keyed by address/size);
-    repeated factorisations of the same host matrix (INLA iterations, the
-    bench's e2e loop) then copy at pinned bandwidth with no staging copy."""
+    """Page-lock a caller-owned values array (keyed by address/size, the
+    array object held so the address cannot be recycled while cached);
+    refactorising the same host values buffer (an INLA loop that rewrites
+    its values array in place, the bench's e2e loop) then copies at pinned
+    bandwidth with no staging copy.  A fresh array pays one registration."""
     key = (vals.ctypes.data, vals.nbytes)
-    if key in _REGISTERED:
+    hit = _REGISTERED.get(key)
+    if hit is not None and hit is vals:
         _REGISTERED.move_to_end(key)
         return True
-    while _REGISTERED and sum(a.nbytes for a in _REGISTERED.values()) + vals.nbytes > _REGISTERED_CAP:
+    if hit is not None:  # same address, different array object: re-register
+        _REGISTERED.pop(key)
+        _lib.lib.tc_host_unregister(_lib.C.c_void_p(key[0]))
+    while _REGISTERED and (len(_REGISTERED) >= _REGISTERED_MAX or
+                           sum(a.nbytes for a in _REGISTERED.values()) + vals.nbytes > _REGISTERED_CAP):
         (p, _), _a = _REGISTERED.popitem(last=False)
         _lib.lib.tc_host_unregister(_lib.C.c_void_p(p))
     if _lib.lib.tc_host_register(_lib.C.c_void_p(key[0]), key[1]) != _lib.TC_OK:
@@ -404,7 +440,15 @@ def logdet_many(problems, opts: FactorOptions | None = None, lanes: int = 4) -> 
     streams = [torch.cuda.Stream() for _ in range(L)]
     for s in streams:  # the result arrays' fill kernels run on the current stream first
         s.wait_stream(torch.cuda.current_stream())
-    staged = [None] * L        # (pinned host, device values, copy-done event) per lane
+    # one pinned + one device staging buffer per lane, sized once for the
+    # largest problem of the batch and allocated before any lane stream runs
+    # (a buffer replaced mid-batch could return to the caching allocator while
+    # the lane's copy/scatter still reads it)
+    cap = max((m.nnz for m in items), default=0)
+    staged = [(torch.empty(max(cap, 1), dtype=torch.float64).pin_memory(),
+               torch.empty(max(cap, 1), dtype=torch.float64, device="cuda"), torch.cuda.Event())
+              for _ in range(min(L, max(P, 1)))]
+    used = [False] * len(staged)
     storages: dict = {}        # (pattern id, lane) -> tile storage
     errors: dict = {}
     pats = [None] * P
@@ -419,14 +463,10 @@ def logdet_many(problems, opts: FactorOptions | None = None, lanes: int = 4) -> 
             continue
         pats[i] = pat
         vals = pat.permuted_values(m)
-        st = staged[lane]
-        if st is None or st[0].numel() < vals.size:
-            st = (torch.empty(vals.size, dtype=torch.float64).pin_memory(),
-                  torch.empty(vals.size, dtype=torch.float64, device="cuda"), torch.cuda.Event())
-            staged[lane] = st
-        else:
-            st[2].synchronize()  # the lane's previous H2D has left the pinned buffer
-        host, dev, ev = st
+        if used[lane]:
+            staged[lane][2].synchronize()  # the lane's previous H2D has left the pinned buffer
+        used[lane] = True
+        host, dev, ev = staged[lane]
         host[: vals.size].copy_(torch.from_numpy(np.ascontiguousarray(vals, dtype=np.float64)))
         key = (id(pat.plan), lane)
         if key not in storages:

@@ -1724,12 +1724,23 @@ extern "C" void tc_plan_destroy(tc_plan_t p) {
 // copy that does not depend on the caller knowing the pointer is registered.
 extern "C" int tc_host_register(void* ptr, size_t bytes) {
     if (!ptr || !bytes) return set_err(TC_ERR_ARG, "host_register: bad arguments");
-    CK(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault));
+    const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterDefault);
+    if (e != cudaSuccess) {
+        // already registered / read-only mapping / overlapping range: the
+        // caller falls back to a staging copy; clear the sticky last-error
+        // slot so a later CK(cudaGetLastError()) does not report it
+        cudaGetLastError();
+        return set_err(TC_ERR_CUDA, "cudaHostRegister: %s", cudaGetErrorString(e));
+    }
     return TC_OK;
 }
 extern "C" int tc_host_unregister(void* ptr) {
     if (!ptr) return set_err(TC_ERR_ARG, "host_unregister: null");
-    CK(cudaHostUnregister(ptr));
+    const cudaError_t e = cudaHostUnregister(ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(TC_ERR_CUDA, "cudaHostUnregister: %s", cudaGetErrorString(e));
+    }
     return TC_OK;
 }
 extern "C" int tc_memcpy_h2d_async(void* dst_dev, const void* src_host, size_t bytes, void* stream) {

@@ -159,12 +159,24 @@ def factor_column_counts(m: SymmetricCsc, p: Permutation | None = None) -> np.nd
     return out
 
 
-def select_ordering(m: SymmetricCsc, candidates: list[Permutation]) -> Permutation:
+def select_ordering(m: SymmetricCsc, candidates) -> Permutation:
     """Identity unless a candidate has a strictly smaller factor; earlier
-    candidates win ties (reference ordering.py:266-275)."""
+    candidates win ties (reference ordering.py:266-275).
+
+    ``candidates`` may also hold zero-argument callables producing a
+    Permutation: they are evaluated in order only while a strictly smaller
+    factor is still possible.  nnz(L) of any symmetric permutation is at least
+    nnz(lower A) (L's pattern contains PAP^T's), so when the identity has zero
+    fill no candidate can win and none is computed -- the result is the one
+    the reference's eager evaluation returns (e.g. BASELINE C1/C4, survey §8(a)
+    row 8), without an RCM of a 2.5e9-entry pattern."""
     best = Permutation.identity(m.n)
     best_nnz = symbolic_fill_count(m, None).nnz_factor
     for cand in candidates:
+        if best_nnz <= m.nnz:
+            break
+        if callable(cand):
+            cand = cand()
         c = symbolic_fill_count(m, cand).nnz_factor
         if c < best_nnz:
             best, best_nnz = cand, c

@@ -73,7 +73,6 @@ class DevicePlan:
         check("tc_plan_create", lib.tc_plan_create(self.n, self.nt, self.S, ptr(r, i32p), ptr(c, i32p),
                                                    C.byref(opts), C.byref(h)))
         self.h = h
-        self._offsets = {}
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -95,15 +94,12 @@ class DevicePlan:
         return torch.empty((self.S, self.nt, self.nt), dtype=torch.float64, device="cuda")
 
     def offsets_for(self, m) -> np.ndarray:
-        """Flat storage offsets of m's stored scalars (host, cached per pattern)."""
-        key = (m.col_ptr.ctypes.data, m.row_idx.ctypes.data, m.nnz)
-        off = self._offsets.get(key)
-        if off is None:
-            off = np.empty(m.nnz, dtype=np.int64)
-            cp, ri = _lib.i64arr(m.col_ptr), _lib.i32arr(m.row_idx)
-            check("tc_plan_pack_offsets", lib.tc_plan_pack_offsets(self.h, m.n, ptr(cp, i64p), ptr(ri, i32p),
-                                                                   ptr(off, i64p)))
-            self._offsets = {key: off}
+        """Flat storage offsets of m's stored scalars (host).  Not cached here:
+        the caller (api._Pattern) owns the pattern and caches its offsets."""
+        off = np.empty(m.nnz, dtype=np.int64)
+        cp, ri = _lib.i64arr(m.col_ptr), _lib.i32arr(m.row_idx)
+        check("tc_plan_pack_offsets", lib.tc_plan_pack_offsets(self.h, m.n, ptr(cp, i64p), ptr(ri, i32p),
+                                                               ptr(off, i64p)))
         return off
 
     def pack_lincomb(self, basis_dev, coef, offsets_dev, storage, stream: int) -> None:

@@ -174,3 +174,33 @@ def test_inla_lincomb_is_bitwise_values():
         for c, b in zip(coef[1:], basis[1:]):
             v = v + c * b
         assert np.array_equal(v, fam.values(*th))
+
+
+def test_experimental_modes_are_gated(monkeypatch):
+    """occupancy=2 / concurrent>1 showed rare logdet drift:
+    rejected unless TILECHOL_EXPERIMENTAL=1."""
+    import pytest
+    from paper_2501_02483_b200.api import FactorOptions
+    monkeypatch.delenv("TILECHOL_EXPERIMENTAL", raising=False)
+    FactorOptions(occupancy=1, concurrent=1)
+    for kw in ({"occupancy": 2}, {"concurrent": 2}):
+        with pytest.raises(ValueError, match="experimental"):
+            FactorOptions(**kw)
+    with pytest.raises(ValueError):
+        FactorOptions(occupancy=3)
+    monkeypatch.setenv("TILECHOL_EXPERIMENTAL", "1")
+    FactorOptions(occupancy=2, concurrent=4)
+
+
+def test_select_ordering_zero_fill_short_circuit():
+    """Zero-fill identity: lazy candidates are never evaluated and the result
+    is identity, as the reference's eager policy returns (ordering.py:266-275)."""
+    from paper_2501_02483_b200 import matcore, ordering
+    m = matcore.generate_arrowhead(matcore.ArrowheadSpec(n=300, b=10, t=5, seed=0))
+    called = []
+
+    def cand():
+        called.append(1)
+        return ordering.Permutation.identity(m.n)
+    p = ordering.select_ordering(m, [cand, cand])
+    assert p.is_identity() and not called
