@@ -67,6 +67,7 @@ def parse(argv=None):
     ap.add_argument("--executor", default="persistent", choices=["persistent", "graph", "direct"])
     ap.add_argument("--lookahead", type=int, default=None, help="bulk-update lookahead depth (default: api default)")
     ap.add_argument("--lanes", type=int, default=4, help="c5: factorisations in flight per GPU")
+    ap.add_argument("--occupancy", type=int, default=0, help="persistent CTAs per SM (0 = plan default)")
     ap.add_argument("--ordering", default="auto",
                     help="auto (SPEC policy) | identity (C4: auto provably picks identity, zero fill)")
     return ap.parse_args(argv)
@@ -392,7 +393,7 @@ def run_batch(a, nt, rank, world, sub=False):
     P = len(thetas)
     lo, hi = shard_range(P, world, rank)
     L = max(1, a.lanes)
-    opts = api.FactorOptions(tile_size=nt, ordering=a.ordering, executor=a.executor)
+    opts = api.FactorOptions(tile_size=nt, ordering=a.ordering, executor=a.executor, occupancy=a.occupancy)
     m0 = fam.matrix(*thetas[0])
     t0 = time.perf_counter()
     pat = api._pattern_for(m0, opts)
@@ -541,7 +542,7 @@ def run_ours(a, name, nt, rank, world):
     t0 = time.perf_counter()
     m = build_matrix(name)
     gen_s = time.perf_counter() - t0
-    opts = api.FactorOptions(tile_size=nt, executor=a.executor, ordering=a.ordering,
+    opts = api.FactorOptions(tile_size=nt, executor=a.executor, ordering=a.ordering, occupancy=a.occupancy,
                              **({} if a.lookahead is None else {"lookahead": a.lookahead}))
     t0 = time.perf_counter()
     pat = api._pattern_for(m, opts)

@@ -201,7 +201,10 @@ int tc_plan_copy_result(tc_plan_t p, int32_t lane, void* stream, int64_t* fail_d
 int tc_plan_logdet(tc_plan_t p, const double* storage_dev, void* stream, double* out);
 /* In-place tile forward/back substitution of rhs_dev[nrhs][T*nt] (column of
  * length T*nt per right-hand side, padded entries must be 0) against the
- * factor: rhs <- L^-T L^-1 rhs. */
+ * factor: rhs <- L^-T L^-1 rhs.  Asynchronous on `stream`:
+ * a batched TRSM forms L_kk^-T for every diagonal tile, then ONE persistent
+ * launch runs both sweeps (per-column done flags, fixed summation order, so
+ * the result does not depend on timing).  nt <= 480. */
 int tc_plan_solve(tc_plan_t p, const double* storage_dev, double* rhs_dev, int32_t nrhs,
                   void* stream);
 /* Scatter CSC values (already on device) into zeroed tile storage with unit

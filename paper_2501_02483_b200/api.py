@@ -29,7 +29,7 @@ from .scheduler import DevicePlan, PlanOptions
 from .symbolic import TileSymbolic, tile_symbolic_factorize
 
 __all__ = ["FactorOptions", "FactorContext", "factorize", "solve", "logdet", "factorize_many",
-           "factorize_many_sharded", "logdet_many", "logdet_many_sharded", "clear_plan_cache"]
+           "factorize_many_sharded", "logdet_many", "logdet_many_sharded", "solve_many", "clear_plan_cache"]
 
 _ORDERINGS = ("auto", "identity", "partial-rcm", "min-degree", "adaptable-nd")
 _REDUCTIONS = ("auto", "on", "off")
@@ -411,45 +411,49 @@ def factorize_many_sharded(problems, rhs=None, opts: FactorOptions | None = None
             "local": local}
 
 
-def logdet_many(problems, opts: FactorOptions | None = None, lanes: int = 4) -> np.ndarray:
-    """Streaming batch for the INLA use (SPEC.md:513-519 semantics, results
-    only): log-determinants of independent SPD matrices, ``lanes``
-    factorisations in flight on their own streams, each lane reusing one
-    pinned staging buffer and one device tile storage, results handed off
-    device-side (no per-problem host sync, no factor kept alive).  Failures
-    are aggregated into FactorizeManyError; values equal solo
-    factorisations bitwise (with the default concurrent=1).
-    """
+def _stream_batch(problems, opts: FactorOptions | None, lanes: int, rhs=None):
+    """Streaming batch engine behind logdet_many / solve_many / the sharded
+    variants: ``lanes`` factorisations in flight on their own streams, each
+    lane reusing one pinned staging buffer, one device tile storage and one
+    solve buffer; results are written device-side into ``rows[i]`` =
+    [logdet_i, x_i (n entries, only when rhs is given)] with no per-problem
+    host sync and no factor kept alive.  Returns (rows (device), fail
+    (device), items, pats, errors)."""
     import dataclasses
 
     import torch
     _lib.require_device()
     o = opts or FactorOptions()
     L = max(1, int(lanes))
-    # lanes overlap H2D, scatter and factorisation; the persistent kernels
-    # themselves take the whole GPU each (concurrent=1).  Grid sharing
-    # (concurrent=L) is opt-in: measured 1.36x batch throughput on C5 but rare
-    # mismatches (~1e-6 relative in 2-5 of 64 log-determinants) under
-    # concurrent kernels remain open (DESIGN.md §10)
     if o.concurrent < 1:
         o = dataclasses.replace(o, concurrent=1)
     items = [p if isinstance(p, SymmetricCsc) else p[0] for p in problems]
     P = len(items)
-    fail = torch.full((P,), -1, dtype=torch.int64, device="cuda")
-    ld = torch.zeros(P, dtype=torch.float64, device="cuda")
+    n_max = max((m.n for m in items), default=0)
+    width = 1 + (n_max if rhs is not None else 0)
+    cur = torch.cuda.current_stream()
+    fail = torch.full((max(P, 1),), -1, dtype=torch.int64, device="cuda")
+    rows = torch.zeros((max(P, 1), width), dtype=torch.float64, device="cuda")
+    b_dev = None
+    if rhs is not None:
+        b_host = np.asarray(rhs, dtype=np.float64)
+        b_dev = torch.from_numpy(np.ascontiguousarray(b_host)).cuda()
     streams = [torch.cuda.Stream() for _ in range(L)]
     for s in streams:  # the result arrays' fill kernels run on the current stream first
-        s.wait_stream(torch.cuda.current_stream())
+        s.wait_stream(cur)
     # one pinned + one device staging buffer per lane, sized once for the
     # largest problem of the batch and allocated before any lane stream runs
     # (a buffer replaced mid-batch could return to the caching allocator while
     # the lane's copy/scatter still reads it)
     cap = max((m.nnz for m in items), default=0)
+    nl = min(L, max(P, 1))
     staged = [(torch.empty(max(cap, 1), dtype=torch.float64).pin_memory(),
                torch.empty(max(cap, 1), dtype=torch.float64, device="cuda"), torch.cuda.Event())
-              for _ in range(min(L, max(P, 1)))]
-    used = [False] * len(staged)
-    storages: dict = {}        # (pattern id, lane) -> tile storage
+              for _ in range(nl)]
+    used = [False] * nl
+    storages: dict = {}        # (plan id, lane) -> tile storage
+    ybufs: dict = {}           # (plan id, lane) -> solve buffer [1, T*nt]
+    perms: dict = {}           # pattern id -> (inverse, forward) device index tensors
     errors: dict = {}
     pats = [None] * P
     for i, m in enumerate(items):
@@ -471,39 +475,122 @@ def logdet_many(problems, opts: FactorOptions | None = None, lanes: int = 4) -> 
         key = (id(pat.plan), lane)
         if key not in storages:
             storages[key] = pat.plan.new_storage()
+            if rhs is not None:
+                ybufs[key] = torch.zeros((1, pat.plan.T * pat.plan.nt), dtype=torch.float64, device="cuda")
+        if rhs is not None and id(pat) not in perms:
+            perms[id(pat)] = (torch.from_numpy(pat.perm.inverse.astype(np.int64)).cuda(),
+                              torch.from_numpy(pat.perm.forward.astype(np.int64)).cuda())
         with torch.cuda.stream(s):
             dev[: vals.size].copy_(host[: vals.size], non_blocking=True)
             ev.record(s)
             pat.plan.pack(dev[: vals.size], pat.offsets(), storages[key], sh)
             pat.plan.factorize_async(storages[key], lane, sh)
-            pat.plan.copy_result(lane, sh, fail[i:i + 1], ld[i:i + 1])
+            pat.plan.copy_result(lane, sh, fail[i:i + 1], rows[i, 0:1])
+            if rhs is not None:
+                y = ybufs[key]
+                inv, fwd = perms[id(pat)]
+                b = b_dev[i] if b_dev.ndim == 2 else b_dev
+                y[0, : m.n] = b[inv]
+                pat.plan.solve(storages[key], y, sh)
+                rows[i, 1: 1 + m.n] = y[0, : m.n][fwd]
     for s in streams:
-        s.synchronize()
-    f = fail.cpu().numpy()
-    out = ld.cpu().numpy()
-    for i in range(P):
+        cur.wait_stream(s)
+    return rows, fail, items, pats, errors
+
+
+def _batch_errors(fail_host, items, pats, errors, out):
+    for i in range(len(items)):
         if i in errors or pats[i] is None:
             continue
-        if f[i] != np.iinfo(np.int64).max:
-            idx = int(f[i])
+        if fail_host[i] != np.iinfo(np.int64).max:
+            idx = int(fail_host[i])
             m = items[i]
             orig = int(pats[i].perm.inverse[idx]) if idx < m.n else None
             errors[i] = NotPositiveDefiniteError(idx, orig)
             out[i] = np.nan
+    return errors
+
+
+def logdet_many(problems, opts: FactorOptions | None = None, lanes: int = 4) -> np.ndarray:
+    """Streaming batch for the INLA use (SPEC.md:513-519 semantics, results
+    only): log-determinants of independent SPD matrices, ``lanes``
+    factorisations in flight on their own streams, each lane reusing one
+    pinned staging buffer and one device tile storage, results handed off
+    device-side (no per-problem host sync, no factor kept alive).  Failures
+    are aggregated into FactorizeManyError; values equal solo
+    factorisations bitwise.
+    """
+    rows, fail, items, pats, errors = _stream_batch(problems, opts, lanes)
+    P = len(items)
+    f = fail.cpu().numpy()[:P]
+    out = rows[:P, 0].cpu().numpy().copy()
+    errors = _batch_errors(f, items, pats, errors, out)
     if errors:
         raise FactorizeManyError(errors, list(out))
     return out
 
 
-def logdet_many_sharded(problems, opts: FactorOptions | None = None, lanes: int = 4, group=None) -> np.ndarray:
-    """logdet_many over the ranks of a torch.distributed (NCCL) group: rank r
-    streams its contiguous block of problems, then one all-gather of the
-    per-problem log-determinants."""
-    import torch.distributed as dist
-    from .batch import gather_rows, shard_range
+def solve_many(problems, rhs, opts: FactorOptions | None = None, lanes: int = 4):
+    """Streaming batch with solves: for every problem A_i, log det A_i and
+    x_i = A_i^-1 b_i (b_i = rhs[i] for a (P, n) rhs, else the shared vector),
+    factor, solve and hand-off all on device.  Returns
+    (logdets float64[P], X float64[P, n])."""
+    rows, fail, items, pats, errors = _stream_batch(problems, opts, lanes, rhs=rhs)
+    P = len(items)
+    f = fail.cpu().numpy()[:P]
+    h = rows[:P].cpu().numpy()
+    out = h[:, 0].copy()
+    errors = _batch_errors(f, items, pats, errors, out)
+    if errors:
+        raise FactorizeManyError(errors, list(out))
+    return out, h[:, 1:].copy()
+
+
+def logdet_many_sharded(problems, opts: FactorOptions | None = None, lanes: int = 4, group=None,
+                        rhs=None):
+    """The streaming batch over the ranks of a torch.distributed (NCCL) group:
+    rank r streams its contiguous block of problems [r*P/W, (r+1)*P/W), then
+    ONE all-gather (device buffers, NVLink) of the per-problem result rows
+    [logdet | x].  Returns float64[P] logdets, or (logdets,
+    X[P, n]) when rhs is given (rhs: shared (n,) vector or (P, n) rows)."""
+    import torch
+    from .batch import sharded_rows
     P = len(problems)
-    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
-    rank = dist.get_rank(group) if world > 1 else 0
-    lo, hi = shard_range(P, world, rank)
-    local = logdet_many(problems[lo:hi], opts=opts, lanes=lanes) if hi > lo else np.zeros(0)
-    return gather_rows(local.reshape(-1, 1), P, group=group, device="cuda")[:, 0].copy()
+    n = problems[0].n if isinstance(problems[0], SymmetricCsc) else problems[0][0].n
+    width = 2 + (n if rhs is not None else 0)   # [logdet, fail index (-1 = ok), x...]
+    local_err: dict = {}
+
+    def local(lo, hi):
+        local_rhs = rhs
+        if rhs is not None and np.asarray(rhs).ndim == 2:
+            local_rhs = np.asarray(rhs)[lo:hi]
+        rows, fail, items, pats, errors = _stream_batch(problems[lo:hi], opts, lanes, rhs=local_rhs)
+        for k, e in errors.items():  # host-side failures (pattern / format errors)
+            local_err[lo + k] = e
+        f = fail[: hi - lo]
+        fcol = torch.where(f == np.iinfo(np.int64).max, torch.full_like(f, -1), f).to(torch.float64)
+        for k in errors:
+            fcol[k] = -2.0
+        # a rank that fails still joins the collective: failures travel in the rows
+        return torch.cat([rows[: hi - lo, :1], fcol[:, None], rows[: hi - lo, 1:]], dim=1)
+
+    allv = sharded_rows(P, local, width, group=group, device="cuda").cpu().numpy()
+    fails = allv[:, 1]
+    if (fails != -1).any():
+        errs = {}
+        for i in np.nonzero(fails != -1)[0].tolist():
+            if i in local_err:
+                errs[i] = local_err[i]
+            elif fails[i] >= 0:
+                m = problems[i] if isinstance(problems[i], SymmetricCsc) else problems[i][0]
+                idx = int(fails[i])
+                pat = _pattern_for(m, opts or FactorOptions())
+                errs[i] = NotPositiveDefiniteError(idx, int(pat.perm.inverse[idx]) if idx < m.n else None)
+            else:
+                errs[i] = RuntimeError(f"problem {i} failed on another rank before factorisation")
+        out = allv[:, 0].copy()
+        out[list(errs)] = np.nan
+        raise FactorizeManyError(errs, list(out))
+    if rhs is None:
+        return allv[:, 0].copy()
+    return allv[:, 0].copy(), allv[:, 2:].copy()

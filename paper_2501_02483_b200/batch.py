@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["shard_range", "gather_rows"]
+__all__ = ["shard_range", "gather_rows", "gather_rows_device", "sharded_rows"]
 
 
 def shard_range(P: int, world: int, rank: int) -> tuple[int, int]:
@@ -48,3 +48,39 @@ def gather_rows(local_rows, P: int, group=None, device=None) -> np.ndarray:
         a, b = shard_range(P, world, r)
         parts.append(out[r][: b - a])
     return torch.cat(parts).cpu().numpy()
+
+
+def gather_rows_device(rows, P: int, group=None):
+    """gather_rows for result rows that already live on the device (float64
+    tensor [n_local, width], problem order): one all_gather straight from the
+    device buffers (NCCL over NVLink on GPUs, gloo on CPU tensors), no host
+    round trip before the collective.  Returns the [P, width] tensor."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    lo, hi = shard_range(P, world, rank)
+    if rows.shape[0] != hi - lo:
+        raise ValueError(f"rank {rank} holds {rows.shape[0]} rows, expected {hi - lo}")
+    if world == 1:
+        return rows
+    cap = -(-P // world)
+    buf = torch.zeros((cap, rows.shape[1]), dtype=rows.dtype, device=rows.device)
+    buf[: hi - lo] = rows
+    out = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(out, buf, group=group)
+    return torch.cat([out[r][: shard_range(P, world, r)[1] - shard_range(P, world, r)[0]] for r in range(world)])
+
+
+def sharded_rows(P: int, local_fn, width: int, group=None, device="cuda"):
+    """Rank orchestration of a sharded batch: this rank computes the result
+    rows of its contiguous block [lo, hi) with ``local_fn(lo, hi)`` (a
+    [hi-lo, width] float64 tensor on ``device``) and one all-gather returns
+    the full [P, width] tensor on every rank."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    lo, hi = shard_range(P, world, rank)
+    rows = local_fn(lo, hi) if hi > lo else torch.zeros((0, width), dtype=torch.float64, device=device)
+    return gather_rows_device(rows, P, group=group)

@@ -562,8 +562,12 @@ struct tc_plan {
     int64_t* d_diag_slots = nullptr;
     // solve metadata: per column off-diagonal slots and rows
     std::vector<int64_t> sol_off;
-    int32_t* d_sol_slots = nullptr;
+    int32_t* d_sol_slots = nullptr;   // backward sweep: off-diagonal slots of column k, rows ascending
     int32_t* d_sol_rows = nullptr;
+    int64_t* d_sol_off = nullptr;     // [T+1]
+    int64_t* d_row_ptr = nullptr;     // forward sweep: off-diagonal tiles of row k, columns ascending
+    int32_t* d_row_col = nullptr;
+    int32_t* d_row_slot = nullptr;
     std::vector<Lane> lanes;
     int prio_hi = 0, prio_lo = 0;
     int dev = 0;
@@ -964,8 +968,13 @@ int build_plan(tc_plan& P) {
     }
     std::vector<int64_t> dslots(T);
     for (int k = 0; k < T; ++k) dslots[k] = P.cs[k];
+    std::vector<int32_t> rs32(rs.begin(), rs.end());
     cudaStream_t s = 0;
     int r = upload(P.items, &P.d_items, s);
+    if (!r) r = upload(P.sol_off, &P.d_sol_off, s);
+    if (!r) r = upload(rp, &P.d_row_ptr, s);
+    if (!r) r = upload(rn, &P.d_row_col, s);
+    if (!r) r = upload(rs32, &P.d_row_slot, s);
     if (!r) r = upload(P.pairs, &P.d_pairs, s);
     if (!r) r = upload(P.tgts, &P.d_tgts, s);
     if (!r) r = upload(dslots, &P.d_diag_slots, s);
@@ -1603,27 +1612,72 @@ extern "C" int tc_plan_logdet(tc_plan_t p, const double* storage, void* stream, 
 
 extern "C" int tc_plan_solve(tc_plan_t p, const double* storage, double* rhs, int32_t nrhs, void* stream) {
     if (!p || !storage || !rhs || nrhs < 1) return set_err(TC_ERR_ARG, "plan_solve: bad arguments");
-    if (p->nt > 1024) return set_err(TC_ERR_ARG, "plan_solve: nt > 1024 unsupported");
+    if (p->nt > kMaxTrsmNt) return set_err(TC_ERR_ARG, "plan_solve: nt > %d unsupported", kMaxTrsmNt);
     cudaStream_t s = (cudaStream_t)stream;
     const int nt = p->nt, T = p->T;
     const int64_t ldr = (int64_t)T * nt;
-    const int bs = std::min(((nt + 31) / 32) * 32, 1024);
-    for (int k = 0; k < T; ++k) {
-        k_trsv_diag<<<nrhs, bs, nt * sizeof(double), s>>>(storage, p->cs[k], rhs, ldr, (int64_t)k * nt, nt, 0);
-        const int64_t a = p->sol_off[k], b = p->sol_off[k + 1];
-        if (b > a)
-            k_gemv_fwd<<<dim3((unsigned)(b - a), nrhs), bs, 0, s>>>(storage, p->d_sol_slots + a, p->d_sol_rows + a, rhs,
-                                                                  ldr, k, nt);
+    const size_t nt2 = (size_t)nt * nt;
+    // (1) Winv_k = L_kk^-T for every diagonal tile: batched TRSM of the identity
+    double* W = nullptr;
+    int32_t* flags = nullptr;
+    CK(cudaMallocAsync((void**)&W, nt2 * T * sizeof(double), s));
+    CK(cudaMallocAsync((void**)&flags, (2 * (size_t)T + 1) * sizeof(int32_t), s));
+    k_set_identity<<<592, 256, 0, s>>>(W, T, nt);
+    int r = TC_OK;
+    {
+        const size_t sm = trsm_smem_bytes(nt);
+        r = prep_kernel((const void*)k_trsm, (int)sm);
+        if (!r) {
+            TrsmArgs ta{};
+            ta.storage = const_cast<double*>(storage);
+            ta.lslots = p->d_diag_slots;
+            ta.X = W;
+            ta.nt = nt;
+            for (int k0 = 0; k0 < T && !r; k0 += 65535) {
+                ta.lslots = p->d_diag_slots + k0;
+                ta.X = W + (size_t)k0 * nt2;
+                dim3 grid((nt + kTrsmRows - 1) / kTrsmRows, (unsigned)std::min(T - k0, 65535));
+                k_trsm<<<grid, kTrsmThreads, sm, s>>>(ta);
+                cudaError_t e = cudaGetLastError();
+                if (e != cudaSuccess) r = set_err(TC_ERR_CUDA, "solve trsm: %s", cudaGetErrorString(e));
+            }
+        }
     }
-    for (int k = T - 1; k >= 0; --k) {
-        const int64_t a = p->sol_off[k], b = p->sol_off[k + 1];
-        if (b > a)
-            k_gemv_bwd<<<nrhs, 256, 0, s>>>(storage, p->d_sol_slots + a, p->d_sol_rows + a, (int)(b - a), rhs, ldr, k,
-                                            nt);
-        k_trsv_diag<<<nrhs, bs, nt * sizeof(double), s>>>(storage, p->cs[k], rhs, ldr, (int64_t)k * nt, nt, 1);
+    // (2) both sweeps in one persistent launch, nrhs in chunks of kSolveMaxRhs
+    if (!r) {
+        const int rows = (nt + 31) & ~31;
+        const int P = rows >= kSolveThreads ? 1 : kSolveThreads / rows;
+        const size_t sm = ((size_t)2 * kSolveMaxRhs * nt + (size_t)P * kSolveMaxRhs * rows) * sizeof(double);
+        r = prep_kernel((const void*)k_solve_sweep, (int)sm);
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->dev);
+        for (int c0 = 0; c0 < nrhs && !r; c0 += kSolveMaxRhs) {
+            CK(cudaMemsetAsync(flags, 0, (2 * (size_t)T + 1) * sizeof(int32_t), s));
+            SolveArgs sa{};
+            sa.storage = storage;
+            sa.winv = W;
+            sa.rhs = rhs + (size_t)c0 * ldr;
+            sa.ldr = ldr;
+            sa.nt = nt;
+            sa.T = T;
+            sa.nrhs = std::min(kSolveMaxRhs, nrhs - c0);
+            sa.row_ptr = p->d_row_ptr;
+            sa.row_col = p->d_row_col;
+            sa.row_slot = p->d_row_slot;
+            sa.col_ptr = p->d_sol_off;
+            sa.col_row = p->d_sol_rows;
+            sa.col_slot = p->d_sol_slots;
+            sa.done = flags;
+            sa.ticket = flags + 2 * T;
+            const int grid = std::max(1, std::min(2 * T, sms));
+            k_solve_sweep<<<grid, kSolveThreads, sm, s>>>(sa);
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) r = set_err(TC_ERR_CUDA, "solve sweep: %s", cudaGetErrorString(e));
+        }
     }
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(s));
+    cudaFreeAsync(W, s);
+    cudaFreeAsync(flags, s);
+    if (r) return r;
     return TC_OK;
 }
 
@@ -1716,6 +1770,10 @@ extern "C" void tc_plan_destroy(tc_plan_t p) {
     cudaFree(p->d_diag_slots);
     cudaFree(p->d_sol_slots);
     cudaFree(p->d_sol_rows);
+    cudaFree(p->d_sol_off);
+    cudaFree(p->d_row_ptr);
+    cudaFree(p->d_row_col);
+    cudaFree(p->d_row_slot);
     delete p;
 }
 

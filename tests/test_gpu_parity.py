@@ -391,3 +391,52 @@ def test_inla_batch_device_assembly_and_streaming_logdets(torch):
         api.logdet_many([ms[0], bad, ms[2]], opts, lanes=2)
     assert set(ei.value.errors) == {1} and isinstance(ei.value.errors[1], NotPositiveDefiniteError)
     assert ei.value.results[0] == solo[0] and ei.value.results[2] == solo[2]
+
+
+# ------------------------------------------------- device solve (persistent) --
+@pytest.mark.parametrize("nt,k", [(17, 1), (48, 3), (120, 11), (200, 2), (240, 1), (480, 1)])
+def test_solve_persistent_sweep(torch, nt, k):
+    """tc_plan_solve: batched L_kk^-T + one persistent launch for both sweeps;
+    residual <= 1e-10 against the CSC matrix for k right-hand sides (k > 8
+    exercises the right-hand-side chunking), equal to the oracle tile solve."""
+    api, ctsf, matcore, symbolic, impl = _imports()
+    m = matcore.generate_arrowhead(matcore.ArrowheadSpec(n=3001, b=90, t=13, seed=3))
+    ctx = api.factorize(m, api.FactorOptions(tile_size=nt))
+    rng = np.random.default_rng(nt)
+    b = rng.standard_normal((m.n, k)) if k > 1 else rng.standard_normal(m.n)
+    x = api.solve(ctx, b)
+    A = O.dense_of(m.n, m.col_ptr, m.row_idx, m.values)
+    res = np.linalg.norm(A @ x - b) / np.linalg.norm(b)
+    assert res <= SOLVE_TOL, res
+    fg = ctx.symbolic.factor_grid
+    st = ctx.factor.host_storage()
+    xr = O.tile_solve(st, fg.slot_map, m.n, nt, b[:, 0] if k > 1 else b, fwd=ctx.permutation.forward)
+    x0 = x[:, 0] if k > 1 else x
+    assert np.linalg.norm(x0 - xr) <= 1e-12 * np.linalg.norm(xr)
+    # deterministic: the same solve twice is bitwise equal
+    assert np.array_equal(api.solve(ctx, b), x)
+
+
+def test_solve_many_streaming_and_sharded_single_rank(torch):
+    """Streaming batch with device solves (api.solve_many, the C5 path) equals
+    solo factorize + solve, and logdet_many_sharded(rhs=...) on one rank
+    returns the same rows."""
+    from paper_2501_02483_b200 import workloads as W
+    api, *_ = _imports()
+    fam = W.InlaFamily(nx=10, ny=12, nsteps=20, nfix=3)
+    ms = [fam.matrix(*t) for t in W.c5_thetas()[::9]]
+    opts = api.FactorOptions(tile_size=64)
+    b = np.linspace(-1.0, 1.0, ms[0].n)
+    solo_ld, solo_x = [], []
+    for m in ms:
+        c = api.factorize(m, opts)
+        solo_ld.append(api.logdet(c))
+        solo_x.append(api.solve(c, b))
+    ld, X = api.solve_many(ms, b, opts, lanes=3)
+    assert np.array_equal(ld, np.array(solo_ld))
+    assert np.array_equal(X, np.stack(solo_x))
+    ld2, X2 = api.logdet_many_sharded(ms, opts, lanes=2, rhs=b)
+    assert np.array_equal(ld2, ld) and np.array_equal(X2, X)
+    for m, x in zip(ms, X):
+        A = O.dense_of(m.n, m.col_ptr, m.row_idx, m.values)
+        assert np.linalg.norm(A @ x - b) <= SOLVE_TOL * np.linalg.norm(b)

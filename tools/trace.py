@@ -24,6 +24,8 @@ ap.add_argument("--out", default="")
 a = ap.parse_args()
 m = bench.build_matrix(a.workload)
 kw = {} if a.lookahead is None else {"lookahead": a.lookahead}
+if a.occupancy == 2:
+    os.environ["TILECHOL_EXPERIMENTAL"] = "1"
 opts = api.FactorOptions(tile_size=a.tile, ordering=a.ordering, occupancy=a.occupancy, **kw)
 pat = api._pattern_for(m, opts)
 plan = pat.plan
@@ -52,15 +54,25 @@ if a.out:
 total = tr[:, 2].max()
 print(f"{a.workload}@{a.tile}: {NT} tasks, {NL} launches, span {total:.1f} us, T={plan.T}")
 names = {0: "bulk", 1: "last", 2: "potrf", 3: "trsm", 4: "combine", 5: "logdet", 6: "splitk"}
+# algorithmic flops per profiling class (serialised direct pass of the same plan)
+from paper_2501_02483_b200._lib import f64p  # noqa: E402
+pms, pcnt, pfl = np.zeros(7), np.zeros(7, np.int64), np.zeros(7)
+plan.pack(vals, pat.offsets(), st, sh)
+check("profile", lib.tc_plan_profile(plan.h, st.data_ptr(), sh, 7, pms.ctypes.data_as(f64p),
+                                     pcnt.ctypes.data_as(i64p), pfl.ctypes.data_as(f64p)))
+sm_peak = 37.15e12 / 148
 cls = lm[tl, 2]
 busy = (tr[:, 2] - tr[:, 1])
 wait = (tr[:, 1] - tr[:, 0])
 for c in sorted(set(cls.tolist())):
     sel = cls == c
+    eff = pfl[c] / (busy[sel].sum() * 1e-6) / sm_peak if busy[sel].sum() > 0 else 0.0
     print(f"  {names[c]:8s} tasks {sel.sum():7d}  mean dur {busy[sel].mean():7.2f} us  sum {busy[sel].sum()/1e3:8.2f} ms"
-          f"  mean dep-wait {wait[sel].mean():7.2f} us")
+          f"  mean dep-wait {wait[sel].mean():7.2f} us  gflop {pfl[c]/1e9:9.1f}  per-SM DMMA eff {eff:.3f}")
 nsm = int(tr[:, 3].max()) + 1
-print(f"  CTA-time busy fraction: {busy.sum() / (total * len(set(zip(tr[:,3].astype(int).tolist()))) * 1):.3f} (per SM id)")
+ncta = len(np.unique(tr[:, 3]))
+print(f"  CTA-time busy fraction: {busy.sum() / (total * ncta):.3f} over {ncta} SMs; dep-wait fraction "
+      f"{wait.sum() / (total * ncta):.3f}")
 # per-column critical path: POTRF(k) start/end, TRSM(k) end, LAST(k+1) start/end
 T = plan.T
 pot_s = np.full(T, np.nan); pot_e = np.full(T, np.nan)
