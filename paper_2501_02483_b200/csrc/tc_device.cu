@@ -74,7 +74,7 @@ UpdKernel pick_upd(int nt) {
     if (nt % 64 == 0) return mk_upd<64, 64, 2, 2, 1>();
     if (nt % 80 == 0 && nt % 48 == 0) return mk_upd<80, 48, 2, 2, 1>();
     if (nt % 80 == 0) return mk_upd<80, 40, 2, 1, 2>();
-    if (nt % 40 == 0) return mk_upd<40, 40, 1, 1, 4>();
+    if (nt % 40 == 0 && nt <= 240) return mk_upd<40, 40, 1, 1, 4>();
     if (nt >= 96) return mk_upd<64, 64, 2, 2, 1>();
     return mk_upd<32, 32, 2, 2, 1>();
 }
@@ -127,7 +127,7 @@ PersistKernel pick_persist(int nt, int minb) {
     if (nt % 64 == 0) return mk_persist<64, 64, 2, 2, 2, 0, 24, 32>(minb, nt);
     if (nt % 80 == 0 && nt % 48 == 0) return mk_persist<80, 48, 2, 2, 2, 24>(minb, nt);
     if (nt % 80 == 0) return mk_persist<80, 40, 2, 1, 4, 0, 32>(minb, nt);
-    if (nt % 40 == 0) return mk_persist<40, 40, 1, 1, 8, 0, 24>(minb, nt);
+    if (nt % 40 == 0 && nt <= 240) return mk_persist<40, 40, 1, 1, 8, 0, 24>(minb, nt);
     if (nt >= 96) return mk_persist<64, 64, 2, 2, 2, 0, 24, 32>(minb, nt);
     return mk_persist<32, 32, 2, 2, 2, 0>(minb, nt);
 }
@@ -157,7 +157,25 @@ bool potrf_supported(int nt) {
     return in_smem || nt % 8 == 0;
 }
 
-constexpr int kMaxTrsmNt = 480;
+constexpr int kMaxTrsmNt = 1024;
+
+// direct TRSM kernel for a tile size: 32-row strips, 16-row strips when the
+// 32-row X strip plus two staging buffers would not fit shared memory
+struct TrsmK {
+    void (*fn)(TrsmArgs);
+    int rows;
+    size_t smem;
+};
+TrsmK trsm_direct(int nt) {
+    if (trsm_fits<32>(nt, 225 * 1024)) return TrsmK{k_trsm<32>, 32, trsm_smem_bytes<32>(nt)};
+    return TrsmK{k_trsm<16>, 16, trsm_smem_bytes<16>(nt)};
+}
+size_t trsm_smem_rows(int rows, int nt) {
+    return rows == 64 ? trsm_smem_bytes<64>(nt) : rows == 32 ? trsm_smem_bytes<32>(nt) : trsm_smem_bytes<16>(nt);
+}
+size_t trsm_ring_rows(int rows, int nt, int nb) {
+    return rows == 64 ? trsm_smem_ring<64>(nt, nb) : rows == 32 ? trsm_smem_ring<32>(nt, nb) : trsm_smem_ring<16>(nt, nb);
+}
 
 inline double* tptr(double* st, double* sc, int64_t S, int64_t s, int nt) {
     const size_t nt2 = (size_t)nt * nt;
@@ -209,8 +227,9 @@ int launch_potrf_direct(double* tile, int nt, int32_t* info_dev, const int64_t* 
 int launch_trsm_direct(const double* L, double* X, int nt, int32_t* info_dev, const int64_t* fail, int64_t op_index,
                        int64_t* fail_p, int32_t* fail_info, cudaStream_t s) {
     if (nt > kMaxTrsmNt) return set_err(TC_ERR_ARG, "trsm: nt=%d > %d unsupported", nt, kMaxTrsmNt);
-    const size_t sm = trsm_smem_bytes(nt);
-    int r = prep_kernel((const void*)k_trsm, (int)sm);
+    const TrsmK TK = trsm_direct(nt);
+    const size_t sm = TK.smem;
+    int r = prep_kernel((const void*)TK.fn, (int)sm);
     if (r) return r;
     TrsmArgs ta{};
     ta.L = L;
@@ -222,8 +241,8 @@ int launch_trsm_direct(const double* L, double* X, int nt, int32_t* info_dev, co
     ta.op_index = op_index;
     ta.fail_p = fail_p;
     ta.fail_info = fail_info;
-    dim3 grid((nt + kTrsmRows - 1) / kTrsmRows, 1);
-    k_trsm<<<grid, kTrsmThreads, sm, s>>>(ta);
+    dim3 grid((nt + TK.rows - 1) / TK.rows, 1);
+    TK.fn<<<grid, 4 * TK.rows, sm, s>>>(ta);
     CK(cudaGetLastError());
     return TC_OK;
 }
@@ -518,6 +537,8 @@ struct Launch {
     uint32_t live = 0;           // COMBINE
     int cls = 0;                 // profiling class: 0 bulk, 1 last, 2 potrf, 3 trsm, 4 combine, 5 logdet, 6 split-K chunk
     int small = 0;               // UPD items use the small latency block (L(k) launches)
+    int chain = 0;               // persistent executor: served from the critical-path queue
+    int fused = 0;               // TRSM: streams POTRF(k)'s panels (only the critical tile)
     double flops = 0.0;          // algorithmic flops of this launch
     std::vector<int32_t> deps;
 };
@@ -572,12 +593,15 @@ struct tc_plan {
     int prio_hi = 0, prio_lo = 0;
     int dev = 0;
     // per-column launch ids (persistent ticket order)
-    std::vector<int32_t> colB, colM, colL, colLo, colPot, colTrsm;
+    std::vector<int32_t> colB, colM, colL, colLo, colPot, colTrsm, colTrsmC;
     std::vector<std::vector<int32_t>> colComb, colChunk;
     // persistent executor
     std::vector<PTask> ptasks;
     std::vector<PLaunch> plaunch;
     std::vector<int32_t> p_remaining, p_deps, p_succ_ptr, p_succ;
+    std::vector<int32_t> chain_list, bg_list;  // task ids of the two persistent queues
+    int32_t* d_chain_list = nullptr;
+    int32_t* d_bg_list = nullptr;
     PTask* d_ptasks = nullptr;
     PLaunch* d_plaunch = nullptr;
     int32_t* d_p_init = nullptr;  // [remaining | deps_left] pristine copy
@@ -586,6 +610,7 @@ struct tc_plan {
     size_t persist_smem = 0;
     bool fuse = true;  // persistent executor: TRSM(k) streams POTRF(k)'s panels
     int persist_trsm_ring = 0;  // 0 = auto staging, >0 = strip ring of that many buffers
+    int persist_trsm_rows = 64;  // TRSM strip rows of the persistent executor
     int persist_minb = 2;
     int persist_grid = 0;
     // fused diagonal SYRK: POTRF(k) applies the last update of its diagonal
@@ -705,11 +730,14 @@ int build_plan(tc_plan& P) {
     P.colLo.assign(T, -1);
     P.colPot.assign(T, -1);
     P.colTrsm.assign(T, -1);
+    P.colTrsmC.assign(T, -1);
     P.colComb.assign(T, {});
     P.colChunk.assign(T, {});
     P.items.clear();
     P.tgts.clear();
-    std::vector<int32_t> pnode(T, -1);           // launch finishing column k
+    std::vector<int32_t> pnode(T, -1);           // launch finishing column k (TRSM of the other tiles, or POTRF)
+    std::vector<int32_t> pnodeC(T, -1);          // TRSM of column k's critical tile (row parent(k)), or -1
+    std::vector<int64_t> crit_slot(T, -1);       // that tile's slot
     std::vector<uint32_t> live_mask(S, 0);
     std::vector<std::vector<int32_t>> buf_writer(S);  // per reduced target: last chunk launch per residue
     const double n3 = (double)nt * nt * nt;
@@ -718,6 +746,7 @@ int build_plan(tc_plan& P) {
         std::sort(cols.begin(), cols.end());
         cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
         for (int32_t c : cols) {
+            if (pnodeC[c] >= 0) deps.push_back(pnodeC[c]);  // never pruned
             const int32_t pa = parent[c];
             if (pa >= 0 && std::binary_search(cols.begin(), cols.end(), pa)) continue;
             deps.push_back(pnode[c]);
@@ -832,7 +861,18 @@ int build_plan(tc_plan& P) {
                 small_now = false;
                 L.cnt = (int64_t)P.items.size() - L.off;
                 if (L.cnt > 0) {
-                    L.deps.push_back(pnode[nlast]);
+                    // L_diag reads only the tile (k, nlast): wait for the TRSM
+                    // launch that finishes that tile (the critical one when
+                    // k == parent(nlast)); L_off reads every tile of column nlast
+                    const bool via_crit = diag_part && SBK && crit_slot[nlast] >= 0 &&
+                                          P.frow[crit_slot[nlast]] == k;
+                    if (via_crit) {
+                        L.deps.push_back(pnodeC[nlast]);
+                    } else {
+                        L.deps.push_back(pnode[nlast]);
+                        if (pnodeC[nlast] >= 0) L.deps.push_back(pnodeC[nlast]);
+                    }
+                    if (diag_part) L.chain = 1;
                     if (prev >= 0) L.deps.push_back(prev);
                     const int32_t id = (int32_t)P.launches.size();
                     if (diag_part) {
@@ -878,31 +918,55 @@ int build_plan(tc_plan& P) {
             if (lnode >= 0) L.deps.push_back(lnode);
             for (int32_t x : comb_diag) L.deps.push_back(x);
             L.flops += n3 / 3.0;
+            L.chain = 1;
             pot = (int32_t)P.launches.size();
             P.colPot[k] = pot;
             P.launches.push_back(std::move(L));
         }
         pnode[k] = pot;
+        // TRSM(k), split: the critical tile (parent(k), k) -- the one the next
+        // diagonal tile's last update L_diag(parent(k)) reads -- streams
+        // POTRF(k)'s panels (fused, persistent executor) so the chain
+        // POTRF(k) -> TRSM(p,k) -> L_diag(p) -> POTRF(p) does not wait for
+        // the rest; the other tiles are solved after POTRF(k) from the whole
+        // staged L_kk and only feed later (lookahead) updates
         if (c1 - c0 > 1) {
-            Launch L;
-            L.kind = L_TRSM;
-            L.high = 1;
-            L.cls = 3;
-            L.k = k;
-            L.slot = c0;
-            L.off = (int64_t)P.tgts.size();
-            for (int64_t t = c0 + 1; t < c1; ++t) P.tgts.push_back((int32_t)t);
-            L.cnt = c1 - c0 - 1;
-            L.deps.push_back(pot);
-            if (bnode >= 0) L.deps.push_back(bnode);
-            if (mnode >= 0) L.deps.push_back(mnode);
-            if (lnode >= 0) L.deps.push_back(lnode);
-            if (lnode_off >= 0) L.deps.push_back(lnode_off);
-            for (int32_t x : comb_off) L.deps.push_back(x);
-            L.flops += n3 * (double)(c1 - c0 - 1);
-            pnode[k] = (int32_t)P.launches.size();
-            P.colTrsm[k] = pnode[k];
-            P.launches.push_back(std::move(L));
+            const int32_t pa = P.frow[c0 + 1];
+            const bool has_crit = !P.opts.no_split_trsm && SBK && rp[pa + 1] > rp[pa] && rn[rp[pa + 1] - 1] == k;
+            for (int part = has_crit ? 0 : 1; part < 2; ++part) {
+                const int64_t t0 = part == 0 ? c0 + 1 : (has_crit ? c0 + 2 : c0 + 1);
+                const int64_t t1 = part == 0 ? c0 + 2 : c1;
+                if (t1 <= t0) continue;
+                Launch L;
+                L.kind = L_TRSM;
+                L.high = 1;
+                L.cls = 3;
+                L.k = k;
+                L.slot = c0;
+                L.off = (int64_t)P.tgts.size();
+                for (int64_t t = t0; t < t1; ++t) P.tgts.push_back((int32_t)t);
+                L.cnt = t1 - t0;
+                L.deps.push_back(pot);
+                if (bnode >= 0) L.deps.push_back(bnode);
+                if (mnode >= 0) L.deps.push_back(mnode);
+                if (lnode >= 0) L.deps.push_back(lnode);
+                if (lnode_off >= 0) L.deps.push_back(lnode_off);
+                for (int32_t x : comb_off) L.deps.push_back(x);
+                L.flops += n3 * (double)(t1 - t0);
+                const int32_t id = (int32_t)P.launches.size();
+                if (part == 0) {
+                    L.chain = 1;
+                    L.fused = 1;
+                    pnodeC[k] = id;
+                    crit_slot[k] = c0 + 1;
+                    P.colTrsmC[k] = id;
+                } else {
+                    L.fused = has_crit ? 0 : 1;
+                    pnode[k] = id;
+                    P.colTrsm[k] = id;
+                }
+                P.launches.push_back(std::move(L));
+            }
         }
         // split-K pieces of reduced chains that became ready with column k
         auto& pcs = pieces_at[k];
@@ -1013,7 +1077,7 @@ int build_persistent(tc_plan& P) {
     for (size_t i = 0; i < NL; ++i) {
         const Launch& L = P.launches[i];
         for (int32_t d : L.deps)
-            if (!(fuse && L.kind == L_TRSM && P.launches[d].kind == L_POTRF && P.launches[d].k == L.k))
+            if (!(fuse && L.kind == L_TRSM && L.fused && P.launches[d].kind == L_POTRF && P.launches[d].k == L.k))
                 pdeps[i].push_back(d);
         if (fuse && L.kind == L_LOGDET)
             for (int k = 0; k < T; ++k) pdeps[i].push_back(P.colPot[k]);
@@ -1062,16 +1126,22 @@ int build_persistent(tc_plan& P) {
     }
     const int D = std::max(1, P.opts.lookahead);
     for (int j = 0; j < std::min(D, T); ++j) put(P.colB[j]);
+    // global topological priority order.  With the chain queue the critical
+    // launches (L_diag, diagonal combines, POTRF, critical TRSM) are served
+    // from their own queue as soon as they are runnable, the rest keeps this
+    // order; M(k+1) (feeds L_diag(k+1)) goes before the bulk B(k+D), the
+    // non-critical TRSM(k) (waits for all of POTRF(k)) after it.
     for (int k = 0; k < T; ++k) {
         put(P.colM[k]);
         put(P.colL[k]);
         for (int32_t c : P.colComb[k]) put(c);
         put(P.colPot[k]);
         put(P.colLo[k]);
-        if (fuse) put(P.colTrsm[k]);
+        put(P.colTrsmC[k]);
+        if (fuse && P.colTrsmC[k] < 0) put(P.colTrsm[k]);  // unsplit: the whole TRSM streams
+        if (k + 1 < T) put(P.colM[k + 1]);
         if (k + D < T) put(P.colB[k + D]);
         if (k + 1 < T) put(P.colB[k + 1]);
-        if (k + 1 < T) put(P.colM[k + 1]);
         put(P.colTrsm[k]);
         for (int32_t c : P.colChunk[k]) put(c);
     }
@@ -1090,7 +1160,14 @@ int build_persistent(tc_plan& P) {
     P.ptasks.clear();
     P.p_remaining.assign(NL, 0);
     P.p_deps.assign(NL, 0);
-    const int nrb = (nt + kPersistTrsmRows - 1) / kPersistTrsmRows;
+    // TRSM strip rows: the largest strip whose X block + L staging fits
+    P.persist_trsm_rows = 16;
+    for (int rows : {64, 32})
+        if (trsm_ring_rows(rows, nt, 2) <= 225 * 1024) {
+            P.persist_trsm_rows = rows;
+            break;
+        }
+    const int nrb = (nt + P.persist_trsm_rows - 1) / P.persist_trsm_rows;
     for (int32_t id : order) {
         const Launch& L = P.launches[id];
         const size_t before = P.ptasks.size();
@@ -1116,6 +1193,11 @@ int build_persistent(tc_plan& P) {
         P.p_deps[id] = (int32_t)pdeps[id].size();
     }
     if (P.ptasks.size() > (size_t)INT32_MAX / 2) return set_err(TC_ERR_ARG, "plan: too many tasks");
+    P.chain_list.clear();
+    P.bg_list.clear();
+    const bool use_chain = !P.opts.no_chain_queue;
+    for (size_t t = 0; t < P.ptasks.size(); ++t)
+        (use_chain && P.launches[P.ptasks[t].launch].chain ? P.chain_list : P.bg_list).push_back((int32_t)t);
     P.p_succ_ptr.assign(NL + 1, 0);
     for (size_t i = 0; i < NL; ++i)
         for (int32_t d : pdeps[i]) P.p_succ_ptr[d + 1]++;
@@ -1143,6 +1225,7 @@ int build_persistent(tc_plan& P) {
                 q.kind = 2;
                 q.k = L.k;
                 q.slot = L.slot;
+                q.pad = L.fused;  // streams POTRF(k)'s panels
                 break;
             case L_COMBINE:
                 q.kind = 3;
@@ -1161,6 +1244,8 @@ int build_persistent(tc_plan& P) {
     if (!r) r = upload(init, &P.d_p_init, s0);
     if (!r) r = upload(P.p_succ_ptr, &P.d_succ_ptr, s0);
     if (!r) r = upload(P.p_succ, &P.d_succ, s0);
+    if (!r) r = upload(P.chain_list, &P.d_chain_list, s0);
+    if (!r) r = upload(P.bg_list, &P.d_bg_list, s0);
     if (!r) {
         std::vector<int32_t> xos(P.S, -1);
         for (int k = 0; k < T; ++k)
@@ -1192,13 +1277,14 @@ int build_persistent(tc_plan& P) {
     const PersistKernel K = pick_persist(nt, P.persist_minb);
     if (!K.fn) return set_err(TC_ERR_ARG, "plan: no persistent kernel variant for tile size %d", nt);
     const size_t base = std::max<size_t>({(size_t)K.smem, potrf_smem(nt, &in_smem) + xs_bytes, (size_t)4096});
-    const size_t t_full = trsm_smem_bytes<kPersistTrsmRows>(nt);
+    const int TR = P.persist_trsm_rows;
+    const size_t t_full = trsm_smem_rows(TR, nt);
     P.persist_trsm_ring = getenv("TC_FORCE_TRSM_RING") ? 2 : 0;  // diagnostic: ring staging at any occupancy
     P.persist_smem = std::max(base, t_full);
     if (P.persist_minb == 2 && P.persist_smem > two_per_sm) {
         // fused TRSM stages one strip at a time (1 buffer); unfused needs a ring
         for (int nb : {P.fuse ? 1 : 3, P.fuse ? 1 : 2}) {
-            const size_t t = std::max(base, trsm_smem_ring<kPersistTrsmRows>(nt, nb));
+            const size_t t = std::max(base, trsm_ring_rows(TR, nt, nb));
             if (t <= two_per_sm) {
                 P.persist_trsm_ring = nb < 2 ? 2 : nb;
                 P.persist_smem = t;
@@ -1223,9 +1309,9 @@ int build_persistent(tc_plan& P) {
 
 int run_persistent(tc_plan& P, Lane& ln, cudaStream_t s) {
     const size_t NL = P.launches.size();
-    if (!ln.d_pstate) CK(cudaMalloc(&ln.d_pstate, (2 * NL + 1) * sizeof(int32_t)));
+    if (!ln.d_pstate) CK(cudaMalloc(&ln.d_pstate, (2 * NL + 2) * sizeof(int32_t)));
     CK(cudaMemcpyAsync(ln.d_pstate, P.d_p_init, 2 * NL * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemsetAsync(ln.d_pstate + 2 * NL, 0, sizeof(int32_t), s));
+    CK(cudaMemsetAsync(ln.d_pstate + 2 * NL, 0, 2 * sizeof(int32_t), s));
     if (P.fuse) {
         if (!ln.d_prog) CK(cudaMalloc(&ln.d_prog, (size_t)P.T * sizeof(int32_t)));
         CK(cudaMemsetAsync(ln.d_prog, 0, (size_t)P.T * sizeof(int32_t), s));
@@ -1245,7 +1331,12 @@ int run_persistent(tc_plan& P, Lane& ln, cudaStream_t s) {
     a.deps_left = ln.d_pstate + NL;
     a.succ_ptr = P.d_succ_ptr;
     a.succ = P.d_succ;
-    a.ticket = ln.d_pstate + 2 * NL;
+    a.ticket = ln.d_pstate + 2 * NL;       // background queue
+    a.chain_ticket = ln.d_pstate + 2 * NL + 1;
+    a.chain_list = P.d_chain_list;
+    a.n_chain = (int32_t)P.chain_list.size();
+    a.bg_list = P.d_bg_list;
+    a.n_bg = (int32_t)P.bg_list.size();
     a.nt = P.nt;
     a.W = P.W;
     a.T = P.T;
@@ -1257,7 +1348,8 @@ int run_persistent(tc_plan& P, Lane& ln, cudaStream_t s) {
     a.trace = ln.d_trace;
     a.xctr = P.nfused ? ln.d_xctr : nullptr;
     a.xctr_of_slot = P.d_xctr_of_slot;
-    a.xper = ((P.nt + kPersistTrsmRows - 1) / kPersistTrsmRows) * (kPersistTrsmRows / 8);
+    a.xper = ((P.nt + P.persist_trsm_rows - 1) / P.persist_trsm_rows) * (P.persist_trsm_rows / 8);
+    a.trsm_rows = P.persist_trsm_rows;
     const PersistKernel K = pick_persist(P.nt, P.persist_minb);
     K.fn<<<P.persist_grid, kPersistThreads, P.persist_smem, s>>>(a);
     CK(cudaGetLastError());
@@ -1325,10 +1417,11 @@ int node_params(tc_plan& P, Lane& ln, size_t i, cudaKernelNodeParams& kp, NodeAr
             na.ta.targets = P.d_tgts + L.off;
             na.ta.nt = nt;
             argv[0] = &na.ta;
-            kp.func = (void*)k_trsm;
-            kp.gridDim = dim3((nt + kTrsmRows - 1) / kTrsmRows, (unsigned)L.cnt);
-            kp.blockDim = dim3(kTrsmThreads);
-            kp.sharedMemBytes = (unsigned)trsm_smem_bytes(nt);
+            const TrsmK TK = trsm_direct(nt);
+            kp.func = (void*)TK.fn;
+            kp.gridDim = dim3((nt + TK.rows - 1) / TK.rows, (unsigned)L.cnt);
+            kp.blockDim = dim3(4 * TK.rows);
+            kp.sharedMemBytes = (unsigned)TK.smem;
             break;
         }
         case L_COMBINE: {
@@ -1391,7 +1484,8 @@ int prep_all(tc_plan& P) {
     bool in_smem;
     r = prep_kernel((const void*)k_potrf, (int)potrf_smem(P.nt, &in_smem));
     if (r) return r;
-    return prep_kernel((const void*)k_trsm, (int)trsm_smem_bytes(P.nt));
+    const TrsmK TK = trsm_direct(P.nt);
+    return prep_kernel((const void*)TK.fn, (int)TK.smem);
 }
 
 int build_graph(tc_plan& P, Lane& ln) {
@@ -1625,8 +1719,9 @@ extern "C" int tc_plan_solve(tc_plan_t p, const double* storage, double* rhs, in
     k_set_identity<<<592, 256, 0, s>>>(W, T, nt);
     int r = TC_OK;
     {
-        const size_t sm = trsm_smem_bytes(nt);
-        r = prep_kernel((const void*)k_trsm, (int)sm);
+        const TrsmK TK = trsm_direct(nt);
+        const size_t sm = TK.smem;
+        r = prep_kernel((const void*)TK.fn, (int)sm);
         if (!r) {
             TrsmArgs ta{};
             ta.storage = const_cast<double*>(storage);
@@ -1636,8 +1731,8 @@ extern "C" int tc_plan_solve(tc_plan_t p, const double* storage, double* rhs, in
             for (int k0 = 0; k0 < T && !r; k0 += 65535) {
                 ta.lslots = p->d_diag_slots + k0;
                 ta.X = W + (size_t)k0 * nt2;
-                dim3 grid((nt + kTrsmRows - 1) / kTrsmRows, (unsigned)std::min(T - k0, 65535));
-                k_trsm<<<grid, kTrsmThreads, sm, s>>>(ta);
+                dim3 grid((nt + TK.rows - 1) / TK.rows, (unsigned)std::min(T - k0, 65535));
+                TK.fn<<<grid, 4 * TK.rows, sm, s>>>(ta);
                 cudaError_t e = cudaGetLastError();
                 if (e != cudaSuccess) r = set_err(TC_ERR_CUDA, "solve trsm: %s", cudaGetErrorString(e));
             }
@@ -1759,6 +1854,8 @@ extern "C" void tc_plan_destroy(tc_plan_t p) {
         cudaFree(ln.d_xctr);
     }
     cudaFree(p->d_ptasks);
+    cudaFree(p->d_chain_list);
+    cudaFree(p->d_bg_list);
     cudaFree(p->d_plaunch);
     cudaFree(p->d_p_init);
     cudaFree(p->d_succ_ptr);
