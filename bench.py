@@ -39,9 +39,9 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# default tile per workload (C3/C5: BASELINE's stated 240 is slower than 120
-# on this executor, see profiles/; tile size is swept with --tile)
-DEFAULT_NT = {"c1": 120, "c2": 120, "c3": 120, "c4": 120, "c5": 120}
+# default tile per workload: 128 (128x64 update blocks; the tile sweep in
+# profiles/ compares 120-480); swept with --tile
+DEFAULT_NT = {"c1": 128, "c2": 128, "c3": 128, "c4": 128, "c5": 128}
 N_OF = {"c1": 10_000, "c2": 100_000, "c3": 200_010, "c4": 1_000_000, "c5": 200_010}
 PEAKS_FILE = os.path.join(ROOT, "profiles", "fp64_peaks.json")
 FP64_FALLBACK_TFLOPS = 37.0  # NVIDIA B200 FP64 (tensor) nominal, used only if unmeasured

@@ -73,24 +73,103 @@ nsm = int(tr[:, 3].max()) + 1
 ncta = len(np.unique(tr[:, 3]))
 print(f"  CTA-time busy fraction: {busy.sum() / (total * ncta):.3f} over {ncta} SMs; dep-wait fraction "
       f"{wait.sum() / (total * ncta):.3f}")
-# per-column critical path: POTRF(k) start/end, TRSM(k) end, LAST(k+1) start/end
+# per-column critical path: POTRF(k), the critical TRSM of column k (chain),
+# L_diag(k+1) (chain), M(k+1) and B(k+1)
 T = plan.T
-pot_s = np.full(T, np.nan); pot_e = np.full(T, np.nan)
-trs_s = np.full(T, np.nan); trs_e = np.full(T, np.nan)
-last_s = np.full(T, np.nan); last_e = np.full(T, np.nan)
+kind = lm[tl, 0] & 0xFF
+chain = (lm[tl, 0] >> 8) & 1
+mid = (lm[tl, 0] >> 9) & 1
+sub = (lm[tl, 0] >> 10) & 1
 kk = lm[tl, 1]
-for c, s_arr, e_arr in ((2, pot_s, pot_e), (3, trs_s, trs_e), (1, last_s, last_e)):
-    sel = np.where(cls == c)[0]
-    for k in np.unique(kk[sel]):
-        idx = sel[kk[sel] == k]
-        s_arr[k] = tr[idx, 1].min()
-        e_arr[k] = tr[idx, 2].max()
+
+
+def span(sel):
+    s_arr = np.full(T, np.nan)
+    e_arr = np.full(T, np.nan)
+    idx = np.nonzero(sel)[0]
+    if idx.size:
+        order = np.argsort(kk[idx], kind="stable")
+        idx = idx[order]
+        ks, starts = np.unique(kk[idx], return_index=True)
+        for j, k in enumerate(ks):
+            seg = idx[starts[j]:(starts[j + 1] if j + 1 < len(starts) else len(idx))]
+            s_arr[k] = tr[seg, 1].min()
+            e_arr[k] = tr[seg, 2].max()
+    return s_arr, e_arr
+
+
+pot_s, pot_e = span(cls == 2)
+ct_s, ct_e = span((cls == 3) & (chain == 1) & (sub == 0))
+c2_s, c2_e = span((cls == 3) & (chain == 1) & (sub == 1))
+ld_s, ld_e = span((cls == 1) & (chain == 1) & (sub == 0))
+lc_s, lc_e = span((cls == 1) & (chain == 1) & (sub == 1))
+tr_s, tr_e = span((cls == 3) & (chain == 0))
+lo_s, lo_e = span((cls == 1) & (chain == 0))
+m_s, m_e = span((cls == 0) & (mid == 1))
+b_s, b_e = span((cls == 0) & (mid == 0))
+busy_all = tr[:, 2] - tr[:, 1]
+for nm, sel in (("C1 TRSM", (cls == 3) & (chain == 1) & (sub == 0)), ("C2 TRSM", (cls == 3) & (chain == 1) & (sub == 1)),
+                ("rest TRSM", (cls == 3) & (chain == 0)), ("L_diag", (cls == 1) & (chain == 1) & (sub == 0)),
+                ("L_crit", (cls == 1) & (chain == 1) & (sub == 1)), ("L_off", (cls == 1) & (chain == 0)),
+                ("near N", (cls == 0) & (mid == 1)), ("far B", (cls == 0) & (mid == 0))):
+    if sel.any():
+        print(f"    {nm:10s} tasks {sel.sum():8d} mean dur {busy_all[sel].mean():7.2f} us  p90 {np.percentile(busy_all[sel], 90):7.2f}"
+              f"  mean wait {wait[sel].mean():7.2f}")
 lo, hi = T // 4, 3 * T // 4
-step = np.diff(pot_s)[lo:hi]
-print(f"  column step (POTRF start to next POTRF start), middle half: mean {np.nanmean(step):.2f} us, "
-      f"median {np.nanmedian(step):.2f}")
-print(f"    POTRF duration        {np.nanmean((pot_e - pot_s)[lo:hi]):7.2f} us")
-print(f"    POTRF end -> TRSM end {np.nanmean((trs_e - pot_e)[lo:hi]):7.2f} us")
-print(f"    TRSM end -> LAST(k+1) start {np.nanmean((last_s[1:] - trs_e[:-1])[lo:hi]):7.2f} us")
-print(f"    LAST(k+1) duration    {np.nanmean((last_e - last_s)[lo:hi]):7.2f} us")
-print(f"    LAST end -> POTRF start {np.nanmean((pot_s - last_e)[lo:hi]):7.2f} us")
+sl = slice(lo, hi)
+
+
+def mean(x):
+    return float(np.nanmean(x[sl]))
+
+
+step = np.full(T, np.nan)
+step[:-1] = np.diff(pot_s)
+print(f"  column step (POTRF(k) start -> POTRF(k+1) start), middle half: mean {mean(step):.2f} us")
+print(f"    POTRF(k) duration                      {mean(pot_e - pot_s):7.2f}")
+nxt = lambda x: np.concatenate([x[1:], [np.nan]])  # noqa: E731  value at k+1
+print(f"    POTRF(k) end -> crit TRSM(k) end       {mean(ct_e - pot_e):7.2f}")
+print(f"    crit TRSM(k) end -> L_diag(k+1) start  {mean(nxt(ld_s) - ct_e):7.2f}")
+print(f"    M(k+1) end - crit TRSM(k) end          {mean(nxt(m_e) - ct_e):7.2f}  (>0: M late)")
+print(f"    B(k+1) end - crit TRSM(k) end          {mean(nxt(b_e) - ct_e):7.2f}  (>0: B late)")
+print(f"    L_diag(k+1) duration                   {mean(ld_e - ld_s):7.2f}")
+print(f"    L_crit(k+1) end - crit TRSM(k) end     {mean(nxt(lc_e) - ct_e):7.2f}   C1(k+1) start - POTRF(k+1) start "
+      f"{mean(nxt(ct_s) - nxt(pot_s)):7.2f}")
+print(f"    C2(k) end - POTRF(k) end               {mean(c2_e - pot_e):7.2f}   rest TRSM(k) end - POTRF(k) end "
+      f"{mean(tr_e - pot_e):7.2f}   L_off(k+1) end - POTRF(k) end {mean(nxt(lo_e) - pot_e):7.2f}")
+print(f"    L_diag(k+1) end -> POTRF(k+1) start    {mean(nxt(pot_s) - nxt(ld_e)):7.2f}")
+print(f"    B(k) start - POTRF(k) start            {mean(b_s - pot_s):7.2f}   B(k) duration {mean(b_e - b_s):7.2f}")
+# launch timeline around a middle column (relative to POTRF(kc) start, us)
+kc = T // 2
+t_ref = pot_s[kc]
+lid = np.unique(tl)
+l_s = np.full(NL, np.nan)
+l_e = np.full(NL, np.nan)
+l_n = np.zeros(NL, np.int64)
+order_t = np.argsort(tl, kind="stable")
+tls = tl[order_t]
+bounds = np.searchsorted(tls, np.arange(NL + 1))
+for L in range(NL):
+    seg = order_t[bounds[L]:bounds[L + 1]]
+    if seg.size:
+        l_s[L] = tr[seg, 1].min()
+        l_e[L] = tr[seg, 2].max()
+        l_n[L] = seg.size
+lk = lm[:, 1]
+lkind = lm[:, 0] & 0xFF
+lcls = lm[:, 2]
+lchain = (lm[:, 0] >> 8) & 1
+lmid = (lm[:, 0] >> 9) & 1
+lsub = (lm[:, 0] >> 10) & 1
+print(f"  launch timeline around column {kc} (us rel. to POTRF({kc}) start):")
+for L in np.argsort(l_s):
+    if np.isnan(l_s[L]) or lk[L] < kc - 1 or lk[L] > kc + 2:
+        continue
+    if l_e[L] - t_ref < -300 or l_s[L] - t_ref > 600:
+        continue
+    nm = {(0, 0): "B", (0, 1): "N"}.get((int(lcls[L]), int(lmid[L])), names.get(int(lcls[L]), "?"))
+    if lcls[L] == 1:
+        nm = "L_diag" if lchain[L] and not lsub[L] else ("L_crit" if lchain[L] else "L_off")
+    if lcls[L] == 3:
+        nm = "C1" if lchain[L] and not lsub[L] else ("C2" if lchain[L] else "TRSMr")
+    print(f"    k={lk[L]:5d} {nm:7s} tasks {l_n[L]:4d}  start {l_s[L] - t_ref:9.1f}  end {l_e[L] - t_ref:9.1f}")
