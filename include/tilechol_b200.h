@@ -169,8 +169,6 @@ typedef struct tc_plan_opts {
     int32_t use_graph;      /* 2 = persistent (default), 1 = CUDA graph, 0 = direct launches */
     int32_t reserved[3];    /* [0] 1 = no POTRF->TRSM streaming, [1] persistent CTAs/SM (0 auto),
                                [2] concurrent factorisations sharing the GPU (grid share) */
-    int32_t no_split_trsm;  /* 1 = one TRSM launch per column (no critical-tile split) */
-    int32_t no_chain_queue; /* 1 = persistent executor hands out every task from one ticket queue */
 } tc_plan_opts;
 
 /* Build a plan from the factor tile pattern (slots in (col,row) order, all

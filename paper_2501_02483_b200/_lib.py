@@ -38,8 +38,7 @@ OP_POTRF, OP_SYRK, OP_TRSM, OP_GEMM, OP_GEADD, OP_ZERO = 1, 2, 3, 4, 5, 6
 
 class PlanOpts(C.Structure):
     _fields_ = [("tree_workers", i32), ("tree_threshold", i32), ("chunk", i32),
-                ("lookahead", i32), ("use_graph", i32), ("reserved", i32 * 3),
-                ("no_split_trsm", i32), ("no_chain_queue", i32)]
+                ("lookahead", i32), ("use_graph", i32), ("reserved", i32 * 3)]
 
 
 # name -> (restype, argtypes); every symbol declared in include/tilechol_b200.h

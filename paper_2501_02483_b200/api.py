@@ -61,7 +61,7 @@ class FactorOptions:
     workers: int = 1
     ordering: str = "auto"
     tree_reduction: str = "auto"
-    lookahead: int = 4             # contributing columns updated one launch per column before the last (0/False = off)
+    lookahead: int = 3             # bulk-update lookahead depth in columns (0/False = off)
     executor: str = "persistent"  # persistent | graph | direct
     chunk: int = 0
     occupancy: int = 0             # persistent CTAs per SM (0 = 1; 2 = experimental)

@@ -74,16 +74,14 @@ UpdKernel mk_upd() {
 // Block shape per tile size: blocks that divide nt exactly where possible so
 // no MMA work is wasted on padding (120 -> 40x40, 160/320 -> 80x40,
 // 240/480 -> 80x48), small / odd sizes fall back to predicated 32x32.
-// Large blocks for nt % 128 == 0: 128x64 half tiles (default; 4x2 warps of
-// 32x32, no split-K) or whole 128x128 tiles (TC_UPD_SHAPE=128x128); one CTA
-// per SM.  Measured on C4 @128: 64x64 split-K 931 ms, 128x64 918 ms (bulk
-// tasks at 53% of the per-SM DMMA rate vs 25% for 40x40), 128x128 1262 ms.
+// Large blocks for nt % 128 == 0: 128x64 half tiles (4x2 warps of 32x32, no
+// split-K) or whole 128x128 tiles; TC_UPD_SHAPE=128x64 / 128x128 / 64x64.
 int big_shape(int nt) {
     if (nt % 128 != 0) return 0;
     const char* f = getenv("TC_UPD_SHAPE");
-    if (!f || !strcmp(f, "128x64")) return 1;  // default: half-tile blocks, 4x2 warps of 32x32
-    if (!strcmp(f, "128x128")) return 2;
-    return 0;  // "64x64": the split-K 64x64 shape
+    if (f && !strcmp(f, "128x64")) return 1;
+    if (f && !strcmp(f, "128x128")) return 2;
+    return 0;
 }
 UpdKernel pick_upd(int nt) {
     switch (big_shape(nt)) {
@@ -99,7 +97,7 @@ UpdKernel pick_upd(int nt) {
     if (nt % 64 == 0) return mk_upd<64, 64, 2, 2, 1>();
     if (nt % 80 == 0 && nt % 48 == 0) return mk_upd<80, 48, 2, 2, 1>();
     if (nt % 80 == 0) return mk_upd<80, 40, 2, 1, 2>();
-    if (nt % 40 == 0 && nt <= 240) return mk_upd<40, 40, 1, 1, 4>();
+    if (nt % 40 == 0) return mk_upd<40, 40, 1, 1, 4>();
     if (nt >= 96) return mk_upd<64, 64, 2, 2, 1>();
     return mk_upd<32, 32, 2, 2, 1>();
 }
@@ -163,7 +161,7 @@ PersistKernel pick_persist(int nt, int minb) {
     if (nt % 64 == 0) return mk_persist<64, 64, 2, 2, 2, 0, 24, 32>(minb, nt);
     if (nt % 80 == 0 && nt % 48 == 0) return mk_persist<80, 48, 2, 2, 2, 24>(minb, nt);
     if (nt % 80 == 0) return mk_persist<80, 40, 2, 1, 4, 0, 32>(minb, nt);
-    if (nt % 40 == 0 && nt <= 240) return mk_persist<40, 40, 1, 1, 8, 0, 24>(minb, nt);
+    if (nt % 40 == 0) return mk_persist<40, 40, 1, 1, 8, 0, 24>(minb, nt);
     if (nt >= 96) return mk_persist<64, 64, 2, 2, 2, 0, 24, 32>(minb, nt);
     return mk_persist<32, 32, 2, 2, 2, 0>(minb, nt);
 }
@@ -573,11 +571,6 @@ struct Launch {
     uint32_t live = 0;           // COMBINE
     int cls = 0;                 // profiling class: 0 bulk, 1 last, 2 potrf, 3 trsm, 4 combine, 5 logdet, 6 split-K chunk
     int small = 0;               // UPD items use the small latency block (L(k) launches)
-    int chain = 0;               // persistent executor: served from the critical-path queue
-    int mid = 0;                 // near launch N(k, j) (one lookahead column before the last)
-    int32_t near_col = -1;       // that column
-    int sub = 0;                 // trace tag: L_crit / C2 (the second critical launch of its kind)
-    int fused = 0;               // TRSM: streams POTRF(k)'s panels (only the critical tile)
     double flops = 0.0;          // algorithmic flops of this launch
     std::vector<int32_t> deps;
 };
@@ -589,7 +582,7 @@ struct Lane {
     double* d_scratch = nullptr;
     cudaGraphExec_t exec = nullptr;
     cudaGraph_t graph = nullptr;
-    int32_t* d_pstate = nullptr;  // persistent: [remaining | deps_left | qhead | qtail | qslots]
+    int32_t* d_pstate = nullptr;  // persistent: [remaining | deps_left | ticket]
     int32_t* d_prog = nullptr;    // persistent fused: per-column POTRF panel progress [T]
     int64_t* d_trace = nullptr;   // persistent: per-task timestamps (tc_plan_trace only)
     int32_t* d_xctr = nullptr;    // persistent: fused diagonal SYRK TRSM warp panel flags [T][32]
@@ -632,32 +625,22 @@ struct tc_plan {
     int prio_hi = 0, prio_lo = 0;
     int dev = 0;
     // per-column launch ids (persistent ticket order)
-    std::vector<int32_t> colB, colM, colL, colLc, colLo, colPot, colTrsm, colTrsmC, colTrsmC2;
-    std::vector<std::vector<int32_t>> colN;  // near launches of column k, oldest column first
+    std::vector<int32_t> colB, colM, colL, colLo, colPot, colTrsm;
     std::vector<std::vector<int32_t>> colComb, colChunk;
     // persistent executor
     std::vector<PTask> ptasks;
     std::vector<PLaunch> plaunch;
     std::vector<int32_t> p_remaining, p_deps, p_succ_ptr, p_succ;
-    std::vector<int32_t> q_cls;              // ready-queue bucket per launch
-    std::vector<int32_t> q_off, q_tot;       // per bucket: slot offset, task count
-    int32_t* d_q_off = nullptr;
-    int32_t* d_q_tot = nullptr;
-    int q_nbk = 0;
     PTask* d_ptasks = nullptr;
     PLaunch* d_plaunch = nullptr;
-    int32_t* d_p_init = nullptr;  // pristine executor state (see build_persistent)
-    size_t p_state_len = 0;       // its length in int32
+    int32_t* d_p_init = nullptr;  // [remaining | deps_left] pristine copy
     int32_t* d_succ_ptr = nullptr;
     int32_t* d_succ = nullptr;
     size_t persist_smem = 0;
     bool fuse = true;  // persistent executor: TRSM(k) streams POTRF(k)'s panels
     int persist_trsm_ring = 0;  // 0 = auto staging, >0 = strip ring of that many buffers
-    int persist_trsm_rows = 64;  // TRSM strip rows of the persistent executor
     int persist_minb = 2;
-    int persist_reserved = 0;  // CTAs dedicated to the critical-path queue
-    int persist_urgent = 0;    // CTAs serving only the next urgent_span columns' buckets
-    int persist_urgent_span = 3;
+    int persist_trsm_rows = 64;  // TRSM strip rows of the persistent executor
     int persist_grid = 0;
     // fused diagonal SYRK: POTRF(k) applies the last update of its diagonal
     // tile itself, consuming L(k, n_last) panel by panel from TRSM(n_last)
@@ -772,24 +755,15 @@ int build_plan(tc_plan& P) {
     P.launches.clear();
     P.colB.assign(T, -1);
     P.colM.assign(T, -1);
-    P.colN.assign(T, {});
     P.colL.assign(T, -1);
     P.colLo.assign(T, -1);
-    P.colLc.assign(T, -1);
-    P.colTrsmC2.assign(T, -1);
     P.colPot.assign(T, -1);
     P.colTrsm.assign(T, -1);
-    P.colTrsmC.assign(T, -1);
     P.colComb.assign(T, {});
     P.colChunk.assign(T, {});
     P.items.clear();
     P.tgts.clear();
-    std::vector<int32_t> pnode(T, -1);           // launch finishing column k (TRSM of the other tiles, or POTRF)
-    // critical TRSM launches of column k: C1 solves tile (parent(k), k) --
-    // the one L_diag(parent(k)) reads -- and C2 tile (parent(parent(k)), k),
-    // the one L_crit(parent(k)) reads; both stream POTRF(k)'s panels
-    std::vector<int32_t> pnodeC(T, -1), pnodeC2(T, -1);
-    std::vector<int64_t> crit_slot(T, -1), crit2_slot(T, -1);
+    std::vector<int32_t> pnode(T, -1);           // launch finishing column k
     std::vector<uint32_t> live_mask(S, 0);
     std::vector<std::vector<int32_t>> buf_writer(S);  // per reduced target: last chunk launch per residue
     const double n3 = (double)nt * nt * nt;
@@ -798,8 +772,6 @@ int build_plan(tc_plan& P) {
         std::sort(cols.begin(), cols.end());
         cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
         for (int32_t c : cols) {
-            if (pnodeC[c] >= 0) deps.push_back(pnodeC[c]);  // never pruned
-            if (pnodeC2[c] >= 0) deps.push_back(pnodeC2[c]);
             const int32_t pa = parent[c];
             if (pa >= 0 && std::binary_search(cols.begin(), cols.end(), pa)) continue;
             deps.push_back(pnode[c]);
@@ -821,18 +793,14 @@ int build_plan(tc_plan& P) {
 
     for (int k = 0; k < T; ++k) {
         const int64_t c0 = P.cs[k], c1 = P.cs[k + 1];
-        // lookahead depth D over the contributing columns cc of column k
-        // (ascending): the last one feeds L(k); each of the D-1 before it
-        // feeds its own near launch N(k, j) (one pair per target, ready as
-        // soon as that column is solved); all earlier ones feed the far bulk
-        // update B(k), ready D columns ahead.  A target's launches are
-        // serialised (read-modify-write), so per-column near launches keep a
-        // long B from holding up the last contributions
+        // lookahead depth D: the last contributing column feeds L(k), the
+        // D-1 before it feed M(k), the rest feed the bulk update B(k), so
+        // B(k+D) can run while columns k-1 .. k+D-1 are still in flight
         const int D = P.opts.lookahead;
         const int64_t nctr = rp[k + 1] - rp[k];
         const int32_t nlast = (D > 0 && nctr > 0) ? rn[rp[k + 1] - 1] : -1;
-        const int64_t nnear = (D > 1 && nctr > 1) ? std::min<int64_t>(D - 1, nctr - 1) : 0;
-        const int32_t bcut = nnear > 0 ? rn[rp[k + 1] - 1 - nnear] : (nlast >= 0 ? nlast : INT32_MAX);
+        const int32_t nmid = (D > 1 && nctr > 1) ? rn[std::max<int64_t>(rp[k], rp[k + 1] - D)] : -1;
+        const int32_t bcut = nmid >= 0 ? nmid : (nlast >= 0 ? nlast : INT32_MAX);
         // first pair of target t whose contributing column is >= col
         auto cut = [&](int64_t t, int32_t col) {
             int64_t x = tp1[t];
@@ -864,10 +832,7 @@ int build_plan(tc_plan& P) {
                 P.launches.push_back(std::move(L));
             }
         }
-        P.colN[k].clear();
-        for (int64_t j = nnear; j >= 1; --j) {  // near column cc[-1-j]
-            const int32_t col = rn[rp[k + 1] - 1 - j];
-            const int32_t col_next = rn[rp[k + 1] - j];
+        if (nmid >= 0) {
             Launch L;
             L.kind = L_UPD;
             L.k = k;
@@ -875,7 +840,7 @@ int build_plan(tc_plan& P) {
             std::vector<int32_t> cols;
             for (int64_t t = c0; t < c1; ++t) {
                 if (red_base[t] >= 0) continue;
-                const int64_t p0 = cut(t, col), p1 = cut(t, col_next);
+                const int64_t p0 = cut(t, nmid), p1 = cut(t, nlast);
                 if (p1 > p0) {
                     emit_items(t, p0, p1, (int32_t)t, MODE_SUB);
                     for (int64_t x = p0; x < p1; ++x) cols.push_back(P.fcol[P.pairs[x].b]);
@@ -885,78 +850,48 @@ int build_plan(tc_plan& P) {
             L.cnt = (int64_t)P.items.size() - L.off;
             if (L.cnt > 0) {
                 add_panel_deps(L.deps, cols);
-                const int32_t prev_w = mnode >= 0 ? mnode : bnode;
-                if (prev_w >= 0) L.deps.push_back(prev_w);
-                L.mid = 1;
-                L.near_col = col;
+                if (bnode >= 0) L.deps.push_back(bnode);
                 mnode = (int32_t)P.launches.size();
-                P.colN[k].push_back(mnode);
+                P.colM[k] = mnode;
                 P.launches.push_back(std::move(L));
             }
         }
-        P.colM[k] = mnode;
         const int32_t prev = mnode >= 0 ? mnode : bnode;  // last writer of column k before L(k)
         // L(k): the last contribution.  With small blocks available it is split
-        // into L_diag(k) (the diagonal tile: POTRF(k) waits only on it),
-        // L_crit(k) (the tile (parent(k), k): only the critical TRSM C1(k)
-        // waits on it) -- both small blocks, critical-path queue -- and L_off(k)
-        // (the other off-diagonal targets, regular blocks)
-        int32_t lnode_off = -1, lnode_crit = -1;
+        // into L_diag(k) (the diagonal tile, small blocks: POTRF(k) waits only
+        // on it) and L_off(k) (off-diagonal targets, regular blocks: only
+        // TRSM(k) waits on them, and TRSM streams behind POTRF anyway)
+        int32_t lnode_off = -1;
         if (nlast >= 0) {
-            const int64_t tcrit = (SBK && c1 - c0 > 1) ? c0 + 1 : -1;
-            for (int part = 0; part < 3; ++part) {  // 0 diag, 1 crit, 2 off
-                if (!SBK && part > 0) break;  // unsplit: one launch, regular blocks
+            for (int part = 0; part < 2; ++part) {
+                const bool diag_part = part == 0;
+                if (!SBK && !diag_part) break;  // unsplit: one launch, regular blocks
                 Launch L;
                 L.kind = L_UPD;
                 L.k = k;
                 L.high = 1;
                 L.cls = 1;
                 L.off = (int64_t)P.items.size();
-                small_now = SBK != 0 && part < 2;
+                small_now = SBK != 0 && diag_part;
                 L.small = small_now ? 1 : 0;
-                bool reads_crit = true;  // every (row, nlast) tile read comes from C1/C2(nlast)
-                bool reads_c1 = false, reads_c2 = false;
                 for (int64_t t = c0; t < c1; ++t) {
                     if (red_base[t] >= 0) continue;
-                    if (SBK) {
-                        const int tp = t == c0 ? 0 : (t == tcrit ? 1 : 2);
-                        if (tp != part) continue;
-                    }
+                    if (SBK && ((t == c0) != diag_part)) continue;
                     const int64_t p1 = tp1[t];
                     if (p1 > tp0[t] && P.fcol[P.pairs[p1 - 1].b] == nlast) {
                         emit_items(t, p1 - 1, p1, (int32_t)t, MODE_SUB);
                         L.flops += (P.frow[t] == k ? 1.0 : 2.0) * n3;
-                        const Pair pr = P.pairs[p1 - 1];
-                        for (int32_t sl : {pr.a, pr.b}) {
-                            if (sl == crit_slot[nlast]) reads_c1 = true;
-                            else if (sl == crit2_slot[nlast]) reads_c2 = true;
-                            else reads_crit = false;
-                        }
                     }
                 }
                 small_now = false;
                 L.cnt = (int64_t)P.items.size() - L.off;
                 if (L.cnt > 0) {
-                    // tiles of column nlast it reads: only the critical ones
-                    // (C1 / C2 launches) or any of them (the whole TRSM)
-                    if (SBK && part < 2 && reads_crit) {
-                        if (reads_c1) L.deps.push_back(pnodeC[nlast]);
-                        if (reads_c2) L.deps.push_back(pnodeC2[nlast]);
-                    } else {
-                        L.deps.push_back(pnode[nlast]);
-                        if (pnodeC[nlast] >= 0) L.deps.push_back(pnodeC[nlast]);
-                        if (pnodeC2[nlast] >= 0) L.deps.push_back(pnodeC2[nlast]);
-                    }
-                    if (part < 2 && SBK) L.chain = 1;
+                    L.deps.push_back(pnode[nlast]);
                     if (prev >= 0) L.deps.push_back(prev);
                     const int32_t id = (int32_t)P.launches.size();
-                    if (part == 0) {
+                    if (diag_part) {
                         lnode = id;
                         P.colL[k] = id;
-                    } else if (part == 1) {
-                        L.sub = 1;
-                        lnode_crit = id;
-                        P.colLc[k] = id;
                     } else {
                         lnode_off = id;
                         P.colLo[k] = id;
@@ -997,82 +932,31 @@ int build_plan(tc_plan& P) {
             if (lnode >= 0) L.deps.push_back(lnode);
             for (int32_t x : comb_diag) L.deps.push_back(x);
             L.flops += n3 / 3.0;
-            L.chain = 1;
             pot = (int32_t)P.launches.size();
             P.colPot[k] = pot;
             P.launches.push_back(std::move(L));
         }
         pnode[k] = pot;
-        // TRSM(k), split: the critical tile (parent(k), k) -- the one the next
-        // diagonal tile's last update L_diag(parent(k)) reads -- streams
-        // POTRF(k)'s panels (fused, persistent executor) so the chain
-        // POTRF(k) -> TRSM(p,k) -> L_diag(p) -> POTRF(p) does not wait for
-        // the rest; the other tiles are solved after POTRF(k) from the whole
-        // staged L_kk and only feed later (lookahead) updates
         if (c1 - c0 > 1) {
-            const int32_t pa = P.frow[c0 + 1];
-            const bool split = !P.opts.no_split_trsm && SBK && red_base[c0 + 1] < 0;
-            // C2: tile (parent(pa), k), when it is the next tile of the column
-            const int32_t ppa = P.cs[pa + 1] - P.cs[pa] > 1 ? P.frow[P.cs[pa] + 1] : -1;
-            const bool has_c2 = split && c1 - c0 > 2 && ppa >= 0 && P.frow[c0 + 2] == ppa && red_base[c0 + 2] < 0;
-            const int64_t rest0 = split ? (has_c2 ? c0 + 3 : c0 + 2) : c0 + 1;
-            for (int part = split ? 0 : 2; part < 3; ++part) {
-                int64_t t0, t1;
-                if (part == 0) {
-                    t0 = c0 + 1;
-                    t1 = c0 + 2;
-                } else if (part == 1) {
-                    if (!has_c2) continue;
-                    t0 = c0 + 2;
-                    t1 = c0 + 3;
-                } else {
-                    t0 = rest0;
-                    t1 = c1;
-                }
-                if (t1 <= t0) continue;
-                Launch L;
-                L.kind = L_TRSM;
-                L.high = 1;
-                L.cls = 3;
-                L.k = k;
-                L.slot = c0;
-                L.off = (int64_t)P.tgts.size();
-                for (int64_t t = t0; t < t1; ++t) P.tgts.push_back((int32_t)t);
-                L.cnt = t1 - t0;
-                L.deps.push_back(pot);
-                if (bnode >= 0) L.deps.push_back(bnode);
-                if (mnode >= 0) L.deps.push_back(mnode);
-                if (lnode >= 0) L.deps.push_back(lnode);
-                if (part == 0) {
-                    if (lnode_crit >= 0) L.deps.push_back(lnode_crit);
-                } else {
-                    if (lnode_off >= 0) L.deps.push_back(lnode_off);
-                    if (lnode_crit >= 0) L.deps.push_back(lnode_crit);
-                    for (int32_t x : comb_off) L.deps.push_back(x);
-                }
-                L.flops += n3 * (double)(t1 - t0);
-                const int32_t id = (int32_t)P.launches.size();
-                if (part == 0) {
-                    L.chain = 1;
-                    L.fused = 1;
-                    pnodeC[k] = id;
-                    crit_slot[k] = c0 + 1;
-                    P.colTrsmC[k] = id;
-                } else if (part == 1) {
-                    L.chain = 1;
-                    L.fused = 1;
-                    L.sub = 1;
-                    pnodeC2[k] = id;
-                    crit2_slot[k] = c0 + 2;
-                    P.colTrsmC2[k] = id;
-                } else {
-                    L.fused = split ? 0 : 1;
-                    pnode[k] = id;
-                    P.colTrsm[k] = id;
-                }
-                P.launches.push_back(std::move(L));
-            }
-            if (pnode[k] == pot) pnode[k] = pnodeC2[k] >= 0 ? pnodeC2[k] : pnodeC[k];  // no rest
+            Launch L;
+            L.kind = L_TRSM;
+            L.high = 1;
+            L.cls = 3;
+            L.k = k;
+            L.slot = c0;
+            L.off = (int64_t)P.tgts.size();
+            for (int64_t t = c0 + 1; t < c1; ++t) P.tgts.push_back((int32_t)t);
+            L.cnt = c1 - c0 - 1;
+            L.deps.push_back(pot);
+            if (bnode >= 0) L.deps.push_back(bnode);
+            if (mnode >= 0) L.deps.push_back(mnode);
+            if (lnode >= 0) L.deps.push_back(lnode);
+            if (lnode_off >= 0) L.deps.push_back(lnode_off);
+            for (int32_t x : comb_off) L.deps.push_back(x);
+            L.flops += n3 * (double)(c1 - c0 - 1);
+            pnode[k] = (int32_t)P.launches.size();
+            P.colTrsm[k] = pnode[k];
+            P.launches.push_back(std::move(L));
         }
         // split-K pieces of reduced chains that became ready with column k
         auto& pcs = pieces_at[k];
@@ -1183,7 +1067,7 @@ int build_persistent(tc_plan& P) {
     for (size_t i = 0; i < NL; ++i) {
         const Launch& L = P.launches[i];
         for (int32_t d : L.deps)
-            if (!(fuse && L.kind == L_TRSM && L.fused && P.launches[d].kind == L_POTRF && P.launches[d].k == L.k))
+            if (!(fuse && L.kind == L_TRSM && P.launches[d].kind == L_POTRF && P.launches[d].k == L.k))
                 pdeps[i].push_back(d);
         if (fuse && L.kind == L_LOGDET)
             for (int k = 0; k < T; ++k) pdeps[i].push_back(P.colPot[k]);
@@ -1230,44 +1114,19 @@ int build_persistent(tc_plan& P) {
         auto& pd = pdeps[i];
         pd.erase(std::remove_if(pd.begin(), pd.end(), [&](int32_t d) { return dead[d] != 0; }), pd.end());
     }
-    // Global topological priority order.  With the chain queue the critical
-    // launches (L_diag, diagonal combines, POTRF, critical TRSM) are served
-    // from their own queue as soon as they are runnable; the background work
-    // keeps this order.  Per column k: the column's chain, its off-diagonal
-    // L and TRSM, then the work that column k-1's TRSM made ready, most
-    // urgent first -- the near launches N(c, .) that read column k-1 in
-    // increasing column c, then the far bulk updates B(c) whose last column
-    // is k-1.
-    std::vector<std::vector<int32_t>> ready_at(T + 1);  // background launches keyed by their last-read column
+    const int D = std::max(1, P.opts.lookahead);
+    for (int j = 0; j < std::min(D, T); ++j) put(P.colB[j]);
     for (int k = 0; k < T; ++k) {
-        for (int32_t id : P.colN[k]) ready_at[P.launches[id].near_col].push_back(id);
-    }
-    std::vector<int32_t> b_last(T, -1);
-    for (int k = 0; k < T; ++k) {
-        const int32_t b = P.colB[k];
-        if (b < 0) continue;
-        int32_t last = -1;
-        for (int32_t d : pdeps[b])
-            if (P.launches[d].kind == L_TRSM || P.launches[d].kind == L_POTRF) last = std::max(last, P.launches[d].k);
-        b_last[k] = last;
-    }
-    std::vector<std::vector<int32_t>> b_ready(T + 1);
-    for (int k = 0; k < T; ++k)
-        if (P.colB[k] >= 0) b_ready[b_last[k] < 0 ? 0 : b_last[k] + 1].push_back(P.colB[k]);
-    for (int32_t id : b_ready[0]) put(id);
-    for (int k = 0; k < T; ++k) {
-        for (int32_t id : P.colN[k]) put(id);  // normally placed already (ready earlier)
+        put(P.colM[k]);
         put(P.colL[k]);
-        put(P.colLc[k]);
         for (int32_t c : P.colComb[k]) put(c);
         put(P.colPot[k]);
-        put(P.colTrsmC[k]);
         put(P.colLo[k]);
-        put(P.colTrsmC2[k]);
-        if (fuse && P.colTrsmC[k] < 0) put(P.colTrsm[k]);  // unsplit: the whole TRSM streams
+        if (fuse) put(P.colTrsm[k]);
+        if (k + D < T) put(P.colB[k + D]);
+        if (k + 1 < T) put(P.colB[k + 1]);
+        if (k + 1 < T) put(P.colM[k + 1]);
         put(P.colTrsm[k]);
-        for (int32_t id : ready_at[k]) put(id);
-        for (int32_t id : b_ready[k + 1]) put(id);
         for (int32_t c : P.colChunk[k]) put(c);
     }
     for (size_t i = 0; i < NL; ++i) put((int32_t)i);
@@ -1280,10 +1139,8 @@ int build_persistent(tc_plan& P) {
                 topo = false;
                 break;
             }
-    if (!topo) {
-        if (getenv("TC_DEBUG_ORDER")) fprintf(stderr, "tilechol: persistent ticket order not topological, using creation order\n");
+    if (!topo)
         for (size_t i = 0; i < NL; ++i) order[i] = (int32_t)i;
-    }
     P.ptasks.clear();
     P.p_remaining.assign(NL, 0);
     P.p_deps.assign(NL, 0);
@@ -1320,22 +1177,6 @@ int build_persistent(tc_plan& P) {
         P.p_deps[id] = (int32_t)pdeps[id].size();
     }
     if (P.ptasks.size() > (size_t)INT32_MAX / 2) return set_err(TC_ERR_ARG, "plan: too many tasks");
-    // ready-queue bucket per launch: 0 critical path; else 1 + the column
-    // that needs it (updates of column k: k, TRSM of column k: k + 1), made
-    // monotone along dependencies so a bucket never waits on a higher one
-    P.q_cls.assign(NL, 1);
-    {
-        std::vector<int32_t> key(NL, 0);
-        for (size_t i = 0; i < NL; ++i) {  // creation order is topological
-            const Launch& L = P.launches[i];
-            int32_t kk = L.kind == L_TRSM ? L.k + 1 : (L.kind == L_LOGDET ? T : L.k);
-            for (int32_t d : pdeps[i]) kk = std::max(kk, key[d]);
-            key[i] = std::min(kk, (int32_t)T);
-            const bool chain = L.chain && !P.opts.no_chain_queue;
-            P.q_cls[i] = chain ? 0 : 1 + key[i];
-        }
-    }
-    P.q_nbk = T + 2;
     P.p_succ_ptr.assign(NL + 1, 0);
     for (size_t i = 0; i < NL; ++i)
         for (int32_t d : pdeps[i]) P.p_succ_ptr[d + 1]++;
@@ -1347,14 +1188,9 @@ int build_persistent(tc_plan& P) {
             for (int32_t d : pdeps[i]) P.p_succ[at[d]++] = (int32_t)i;
     }
     P.plaunch.assign(NL, PLaunch{});
-    std::vector<int32_t> first(NL, 0);
-    for (size_t t = P.ptasks.size(); t-- > 0;) first[P.ptasks[t].launch] = (int32_t)t;
     for (size_t i = 0; i < NL; ++i) {
         const Launch& L = P.launches[i];
         PLaunch& q = P.plaunch[i];
-        q.first = first[i];
-        q.ntask = P.p_remaining[i];
-        q.qcls = P.q_cls[i];
         switch (L.kind) {
             case L_UPD: q.kind = 0; break;
             case L_POTRF:
@@ -1368,7 +1204,6 @@ int build_persistent(tc_plan& P) {
                 q.kind = 2;
                 q.k = L.k;
                 q.slot = L.slot;
-                q.pad = L.fused;  // streams POTRF(k)'s panels
                 break;
             case L_COMBINE:
                 q.kind = 3;
@@ -1379,32 +1214,12 @@ int build_persistent(tc_plan& P) {
             default: q.kind = 4; break;
         }
     }
-    // initial executor state [remaining | deps_left | head[nbk] | tail[nbk] | watermark | slots]:
-    // the tasks of launches without dependencies are queued up front
-    const int NBK = P.q_nbk;
-    P.q_tot.assign(NBK, 0);
-    P.q_off.assign(NBK, 0);
-    for (size_t i = 0; i < NL; ++i) P.q_tot[P.q_cls[i]] += P.p_remaining[i];
-    for (int c = 1; c < NBK; ++c) P.q_off[c] = P.q_off[c - 1] + P.q_tot[c - 1];
     std::vector<int32_t> init(P.p_remaining);
     init.insert(init.end(), P.p_deps.begin(), P.p_deps.end());
-    std::vector<int32_t> qtail(NBK, 0), slots(P.ptasks.size(), -1);
-    for (int32_t id : order) {
-        if (dead[id] || P.p_deps[id] != 0 || P.p_remaining[id] == 0) continue;
-        const int c = P.q_cls[id];
-        for (int32_t x = 0; x < P.p_remaining[id]; ++x) slots[P.q_off[c] + qtail[c]++] = first[id] + x;
-    }
-    init.insert(init.end(), NBK, 0);                       // heads
-    init.insert(init.end(), qtail.begin(), qtail.end());   // tails
-    init.push_back(1);                                     // watermark
-    init.insert(init.end(), slots.begin(), slots.end());
     cudaStream_t s0 = 0;
     int r = upload(P.ptasks, &P.d_ptasks, s0);
     if (!r) r = upload(P.plaunch, &P.d_plaunch, s0);
-    P.p_state_len = init.size();
     if (!r) r = upload(init, &P.d_p_init, s0);
-    if (!r) r = upload(P.q_off, &P.d_q_off, s0);
-    if (!r) r = upload(P.q_tot, &P.d_q_tot, s0);
     if (!r) r = upload(P.p_succ_ptr, &P.d_succ_ptr, s0);
     if (!r) r = upload(P.p_succ, &P.d_succ, s0);
     if (!r) {
@@ -1427,9 +1242,6 @@ int build_persistent(tc_plan& P) {
     // DESIGN.md §10) that one CTA per SM has not shown; opt-in until found.
     const int occ_mode = P.opts.reserved[1];
     P.persist_minb = occ_mode == 2 && !big_shape(nt) ? 2 : 1;
-    P.persist_reserved = getenv("TC_RESERVE") ? atoi(getenv("TC_RESERVE")) : 0;
-    P.persist_urgent = getenv("TC_URGENT") ? atoi(getenv("TC_URGENT")) : 0;
-    P.persist_urgent_span = getenv("TC_URGENT_SPAN") ? atoi(getenv("TC_URGENT_SPAN")) : 3;
     bool in_smem;
     // shared memory: the max over task kinds; the fused TRSM may stage L
     // strip by strip (ring) instead of whole when that lets two CTAs share an SM
@@ -1473,8 +1285,9 @@ int build_persistent(tc_plan& P) {
 
 int run_persistent(tc_plan& P, Lane& ln, cudaStream_t s) {
     const size_t NL = P.launches.size();
-    if (!ln.d_pstate) CK(cudaMalloc(&ln.d_pstate, P.p_state_len * sizeof(int32_t)));
-    CK(cudaMemcpyAsync(ln.d_pstate, P.d_p_init, P.p_state_len * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    if (!ln.d_pstate) CK(cudaMalloc(&ln.d_pstate, (2 * NL + 1) * sizeof(int32_t)));
+    CK(cudaMemcpyAsync(ln.d_pstate, P.d_p_init, 2 * NL * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemsetAsync(ln.d_pstate + 2 * NL, 0, sizeof(int32_t), s));
     if (P.fuse) {
         if (!ln.d_prog) CK(cudaMalloc(&ln.d_prog, (size_t)P.T * sizeof(int32_t)));
         CK(cudaMemsetAsync(ln.d_prog, 0, (size_t)P.T * sizeof(int32_t), s));
@@ -1494,16 +1307,7 @@ int run_persistent(tc_plan& P, Lane& ln, cudaStream_t s) {
     a.deps_left = ln.d_pstate + NL;
     a.succ_ptr = P.d_succ_ptr;
     a.succ = P.d_succ;
-    a.qhead = ln.d_pstate + 2 * NL;
-    a.qtail = a.qhead + P.q_nbk;
-    a.qwm = a.qtail + P.q_nbk;
-    a.qslot = a.qwm + 1;
-    a.qoff = P.d_q_off;
-    a.qtot = P.d_q_tot;
-    a.nbk = P.q_nbk;
-    a.n_reserved = P.q_tot[0] == 0 ? 0 : std::min(P.persist_reserved, P.persist_grid / 2);
-    a.n_urgent = std::min(P.persist_urgent, P.persist_grid / 2);
-    a.urgent_span = P.persist_urgent_span;
+    a.ticket = ln.d_pstate + 2 * NL;
     a.nt = P.nt;
     a.W = P.W;
     a.T = P.T;
@@ -1804,7 +1608,7 @@ extern "C" int tc_plan_debug_ticket(tc_plan_t p, int32_t lane, int32_t* ticket, 
     cudaStream_t s;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     const size_t NL = p->launches.size();
-    CK(cudaMemcpyAsync(ticket, p->lanes[lane].d_pstate + 2 * NL, 4, cudaMemcpyDeviceToHost, s));  // class-0 head
+    CK(cudaMemcpyAsync(ticket, p->lanes[lane].d_pstate + 2 * NL, 4, cudaMemcpyDeviceToHost, s));
     if (getenv("TC_DEBUG_DUMP")) {  // remaining/deps + ticket order of every launch -> file
         std::vector<int32_t> st(2 * NL);
         CK(cudaMemcpyAsync(st.data(), p->lanes[lane].d_pstate, 2 * NL * 4, cudaMemcpyDeviceToHost, s));
@@ -2023,8 +1827,6 @@ extern "C" void tc_plan_destroy(tc_plan_t p) {
     cudaFree(p->d_ptasks);
     cudaFree(p->d_plaunch);
     cudaFree(p->d_p_init);
-    cudaFree(p->d_q_off);
-    cudaFree(p->d_q_tot);
     cudaFree(p->d_succ_ptr);
     cudaFree(p->d_succ);
     cudaFree(p->d_xctr_of_slot);
@@ -2160,8 +1962,7 @@ extern "C" int tc_plan_trace(tc_plan_t p, double* storage, void* stream, int64_t
     if (r) return r;
     for (int64_t t = 0; t < NT; ++t) task_launch[t] = p->ptasks[t].launch;
     for (int64_t i = 0; i < NL; ++i) {
-        launch_meta[3 * i] = p->launches[i].kind | (p->launches[i].chain << 8) | (p->launches[i].mid << 9) |
-                               (p->launches[i].sub << 10);
+        launch_meta[3 * i] = p->launches[i].kind;
         launch_meta[3 * i + 1] = p->launches[i].k;
         launch_meta[3 * i + 2] = p->launches[i].cls;
     }

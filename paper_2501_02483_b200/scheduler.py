@@ -37,13 +37,11 @@ class PlanOptions:
     tree_workers: int = 8        # W partial accumulators per long chain
     tree_threshold: int = 0      # 0 = 2*W (reference rule), < 0 = no tree reduction
     chunk: int = 0               # columns per split-K launch (0 = 8)
-    lookahead: int = 4           # near-column launches before the last contribution (0 = off)
+    lookahead: int = 3           # columns of lookahead for the bulk update (0 = off)
     executor: str = "persistent"  # persistent | graph | direct
     occupancy: int = 0            # persistent CTAs per SM: 0 auto (2 when it fits), 1, 2
     fuse_trsm: bool = True        # persistent: TRSM(k) streams POTRF(k)'s panels
     concurrent: int = 1           # persistent: factorisations sharing the GPU (grid share)
-    split_trsm: bool = True       # TRSM(k): critical tile (parent(k), k) in its own streamed launch
-    chain_queue: bool = True      # persistent: critical-path tasks served from a priority queue
 
     def to_c(self) -> PlanOpts:
         o = PlanOpts()
@@ -55,8 +53,6 @@ class PlanOptions:
         o.reserved[0] = 0 if self.fuse_trsm else 1
         o.reserved[1] = int(self.occupancy)
         o.reserved[2] = int(self.concurrent)
-        o.no_split_trsm = 0 if self.split_trsm else 1
-        o.no_chain_queue = 0 if self.chain_queue else 1
         return o
 
 

@@ -30,9 +30,6 @@ vals = torch.from_numpy(np.ascontiguousarray(pat.permuted_values(m))).cuda()
 base = pat.plan.options
 VAR = {
     "default": {},
-    "nochain": {"chain_queue": False},
-    "nosplit": {"split_trsm": False},
-    "neither": {"chain_queue": False, "split_trsm": False},
     "la1": {"lookahead": 1},
     "la3": {"lookahead": 3},
     "la4": {"lookahead": 4},
@@ -42,6 +39,7 @@ VAR = {
     "la12": {"lookahead": 12},
     "la16": {"lookahead": 16},
     "graph": {"executor": "graph"},
+    "la2": {"lookahead": 2},
 }
 st = pat.plan.new_storage()
 sh = torch.cuda.current_stream().cuda_stream

@@ -8,7 +8,7 @@ int main() {
         std::vector<double> h(nt * nt);
         for (int j = 0; j < nt; ++j) for (int i = 0; i < nt; ++i) h[j * nt + i] = (i == j) ? nt + 1.0 : 1.0 / (1 + i + j);
         double* d; cudaMalloc(&d, nt * nt * 8);
-        int ntp = (nt + 7) & ~7; size_t sm = potrf_packed_doubles(ntp) * 8 + ntp * 8;
+        int ntp = (nt + 7) & ~7; size_t sm = potrf_smem_bytes(ntp, true);
         cudaFuncSetAttribute(k_potrf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         PotrfArgs pa{}; pa.tile = d; pa.nt = nt; pa.in_smem = 1;
         float best = 1e9;

@@ -13,7 +13,7 @@ int main(int argc, char** argv) {
     double* d;
     cudaMalloc(&d, nt * nt * 8);
     int ntp = (nt + 7) & ~7;
-    size_t sm = potrf_packed_doubles(ntp) * 8 + ntp * 8;
+    size_t sm = potrf_smem_bytes(ntp, true);
     cudaFuncSetAttribute(k_potrf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     PotrfArgs pa{};
     pa.tile = d;

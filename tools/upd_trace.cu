@@ -36,4 +36,6 @@ int main() {
     run<40, 40, 1, 1, 8>(120, "persist40x40ks8");
     run<40, 40, 1, 1, 4>(120, "direct40x40ks4");
     run<64, 64, 2, 2, 2>(128, "persist64x64ks2");
+    run<128, 64, 4, 2, 1>(128, "persist128x64");
+    run<128, 128, 2, 4, 1>(128, "persist128x128");
 }
