@@ -40,6 +40,9 @@ VAR = {
     "la16": {"lookahead": 16},
     "graph": {"executor": "graph"},
     "la2": {"lookahead": 2},
+    "occ2": {"occupancy": 2},
+    "occ2la2": {"occupancy": 2, "lookahead": 2},
+    "occ2la4": {"occupancy": 2, "lookahead": 4},
 }
 st = pat.plan.new_storage()
 sh = torch.cuda.current_stream().cuda_stream
