@@ -1,0 +1,120 @@
+"""Full-size BASELINE parity on the GPU (VERDICT r1 "what's weak" #2).
+
+Every configuration is factorised at its full size through the public API
+and checked against the parity bars of north_star / SURVEY 8(c):
+
+* backward error ||PAP^T - LL^T||_F / ||A||_F <= 1e-12 by the device replay
+  of the reference op stream (tc_replay_residual, reference
+  _backend_numba.py:136-185) against the packed original;
+* the factor and partial log-determinant of the first K tile columns equal
+  the CPU oracle's (oracle.run_ops over the reference op stream of that
+  prefix, oracle/workloads.prefix_problem) within 1e-12 / 1e-10 -- the whole
+  factor for C2, whose oracle run takes ~3 s;
+* the C5 batch path (lanes, device value assembly) returns the solo
+  log-determinants bitwise.
+
+The oracle is the checker only (tests may import it; the product never does).
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+BACKWARD_TOL = 1e-12
+FACTOR_TOL = 1e-12
+LOGDET_TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    assert t.cuda.is_available()
+    return t
+
+
+def _factor(torch, name, nt, ordering="identity"):
+    import bench
+    from paper_2501_02483_b200 import api
+    m = bench.build_matrix(name)
+    opts = api.FactorOptions(tile_size=nt, ordering=ordering)
+    pat = api._pattern_for(m, opts)
+    vals = torch.from_numpy(np.ascontiguousarray(pat.permuted_values(m))).cuda()
+    offs = pat.offsets()
+    st = pat.plan.new_storage()
+    sh = torch.cuda.current_stream().cuda_stream
+    pat.plan.pack(vals, offs, st, sh)
+    pat.plan.factorize_async(st, 0, sh)
+    fail, ld = pat.plan.collect(0, sh)
+    assert fail < 0, f"{name}@{nt}: false failure at {fail}"
+    return m, pat, vals, offs, st, sh, ld
+
+
+def _prefix_check(name, nt, pat, st, target_flops):
+    import bench
+    pr = bench.oracle_sample(name, nt, target_flops)
+    _, pr["factor"] = bench.time_sample(pr)
+    par = bench.prefix_parity(pat, st, pr, nt)
+    assert par["factor_rel_diff"] <= FACTOR_TOL, par
+    assert par["partial_logdet_rel_diff"] <= LOGDET_TOL, par
+    return par
+
+
+def test_c2_whole_factor_vs_oracle(torch):
+    """C2 (n=100,000 variable band, fill tiles at segment drops): the whole
+    device factor against the oracle's, logdet, backward error."""
+    import bench
+    m, pat, vals, offs, st, sh, ld = _factor(torch, "c2", 128)
+    par = _prefix_check("c2", 128, pat, st, 1e30)  # K = every column
+    assert par["prefix_columns"] == pat.plan.T
+    be = bench.device_backward_error(pat, m, st, vals, offs, sh)
+    assert be["backward_error"] <= BACKWARD_TOL, be
+
+
+@pytest.mark.parametrize("nt", [128, 240])
+def test_c3_full_inla(torch, nt):
+    """C3 (INLA n=200,010, 4,983 fill tiles at nt=240): device backward error
+    and the oracle prefix (~1e11 tile flops)."""
+    import bench
+    m, pat, vals, offs, st, sh, ld = _factor(torch, "c3", nt)
+    assert np.isfinite(ld)
+    be = bench.device_backward_error(pat, m, st, vals, offs, sh)
+    assert be["backward_error"] <= BACKWARD_TOL, be
+    _prefix_check("c3", nt, pat, st, 1e11)
+
+
+def test_c5_thetas_full(torch):
+    """Four C5 hyperparameter points at full size: the streaming batch
+    (device value assembly, lanes) equals solo factorisations bitwise and
+    each solo factor has backward error <= 1e-12."""
+    import bench
+    from paper_2501_02483_b200 import api, workloads as W
+    fam = W.InlaFamily()
+    thetas = W.c5_thetas()[::21][:4]
+    ms = [fam.matrix(*t) for t in thetas]
+    opts = api.FactorOptions(tile_size=128, ordering="identity")
+    batch = np.asarray(api.logdet_many(ms, opts, lanes=2))
+    for m, lb in zip(ms, batch):
+        ctx = api.factorize(m, opts)
+        assert api.logdet(ctx) == lb
+        pat = api._pattern_for(m, opts)
+        vals = torch.from_numpy(np.ascontiguousarray(pat.permuted_values(m))).cuda()
+        sh = torch.cuda.current_stream().cuda_stream
+        be = bench.device_backward_error(pat, m, ctx.factor.storage, vals, pat.offsets(), sh)
+        assert be["backward_error"] <= BACKWARD_TOL, be
+
+
+def test_c4_full_arrowhead(torch):
+    """C4 (n=1,000,000, b=2000, t=500, 2.5e9 nonzeros, 22.5 GB of tiles):
+    device backward error and the oracle prefix (~2e11 tile flops)."""
+    import bench
+    m, pat, vals, offs, st, sh, ld = _factor(torch, "c4", 128)
+    assert np.isfinite(ld)
+    be = bench.device_backward_error(pat, m, st, vals, offs, sh)
+    assert be["backward_error"] <= BACKWARD_TOL, be
+    _prefix_check("c4", 128, pat, st, 2e11)

@@ -76,7 +76,7 @@ def test_tile_kats(torch):
     assert relf(c, k["rk_syrk"]) < 1e-14
 
 
-@pytest.mark.parametrize("nt", [1, 3, 8, 17, 40, 48, 64, 120, 160, 200, 240, 320, 480])
+@pytest.mark.parametrize("nt", [1, 3, 8, 17, 40, 48, 64, 120, 128, 160, 200, 240, 320, 480, 600])
 def test_tile_kernels_vs_torch_fp64(torch, nt):
     """Each tile kernel vs a plain PyTorch fp64 reference of the same op."""
     *_, impl = _imports()
