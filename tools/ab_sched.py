@@ -39,6 +39,7 @@ VAR = {
     "la12": {"lookahead": 12},
     "la16": {"lookahead": 16},
     "graph": {"executor": "graph"},
+    "direct": {"executor": "direct"},
     "la2": {"lookahead": 2},
     "occ2": {"occupancy": 2},
     "occ2la2": {"occupancy": 2, "lookahead": 2},
