@@ -188,7 +188,7 @@ size_t potrf_smem(int nt, bool* in_smem) {
 bool potrf_supported(int nt) {
     bool in_smem;
     potrf_smem(nt, &in_smem);
-    return in_smem || nt % 8 == 0;
+    return in_smem || (nt % 8 == 0 && nt <= 768);  // in place: 8-row blocks, <= 96 of them
 }
 
 constexpr int kMaxTrsmNt = 1024;
@@ -1074,11 +1074,11 @@ int build_persistent(tc_plan& P) {
         std::sort(pdeps[i].begin(), pdeps[i].end());
         pdeps[i].erase(std::unique(pdeps[i].begin(), pdeps[i].end()), pdeps[i].end());
     }
-    // Fused diagonal SYRK (packed in-smem POTRF only): the diagonal tile's
-    // items leave L(k); POTRF(k) no longer waits for L(k) but streams the
-    // published panels of L(k, n_last) (TRSM(n_last) is ticketed earlier).
-    // L(k) keeps the off-diagonal targets (TRSM(k) still depends on it); an
-    // L(k) left empty is dropped from the DAG.
+    // Fused diagonal SYRK (packed in-smem POTRF, nt <= 128): the diagonal
+    // tile's one-pair items leave L(k); POTRF(k) applies A(k,k) -= X X^T with
+    // X = L(k, n_last) itself and waits for the TRSM launch of column n_last
+    // instead of L(k) -- one hand-off and one dispatch fewer on the column
+    // chain.  L(k) keeps any other targets; an L(k) left empty is dropped.
     std::vector<int64_t> loff(NL), lcnt(NL);
     for (size_t i = 0; i < NL; ++i) {
         loff[i] = P.launches[i].off;
@@ -1089,9 +1089,11 @@ int build_persistent(tc_plan& P) {
     P.nfused = 0;
     bool pin_smem;
     potrf_smem(nt, &pin_smem);
-    // experimental (off by default: the per-panel TRSM publication costs more
-    // than the LAST hand-off it removes); TC_SYRK_FUSE=1 enables
-    const bool fuse_syrk = TC_SYRK_FUSE_CODE && pin_smem && getenv("TC_SYRK_FUSE") != nullptr;
+    // compiled out (TC_SYRK_FUSE_CODE): the in-CTA SYRK made POTRF 23 us
+    // longer, more than the L_diag hand-off it removes (C4@128 551 vs 524 ms,
+    // C2 49.6 vs 38.8 ms)
+    const bool fuse_syrk = TC_SYRK_FUSE_CODE && pin_smem && ((nt + 7) & ~7) <= 128 && getenv("TC_SYRK_FUSE") &&
+                           atoi(getenv("TC_SYRK_FUSE")) == 1;
     for (int k = 0; k < T && fuse_syrk; ++k) {
         const int32_t lk = P.colL[k];
         if (lk < 0) continue;
@@ -1109,6 +1111,10 @@ int build_persistent(tc_plan& P) {
         if (lcnt[lk] == 0) dead[lk] = 1;
         auto& pd = pdeps[P.colPot[k]];
         pd.erase(std::remove(pd.begin(), pd.end(), lk), pd.end());
+        const int32_t src = P.fcol[pr.a];  // X's column: POTRF(k) reads its TRSM output
+        pd.push_back(P.colTrsm[src] >= 0 ? P.colTrsm[src] : P.colPot[src]);
+        std::sort(pd.begin(), pd.end());
+        pd.erase(std::unique(pd.begin(), pd.end()), pd.end());
     }
     for (size_t i = 0; i < NL; ++i) {
         auto& pd = pdeps[i];
@@ -1260,7 +1266,7 @@ int build_persistent(tc_plan& P) {
     bool in_smem;
     // shared memory: the max over task kinds; the fused TRSM may stage L
     // strip by strip (ring) instead of whole when that lets two CTAs share an SM
-    const size_t xs_bytes = P.nfused ? (size_t)8 * pad_ld((nt + 7) & ~7) * sizeof(double) : 0;
+    const size_t xs_bytes = P.nfused ? (size_t)2 * 16 * pad_ld((nt + 7) & ~7) * sizeof(double) : 0;
     const size_t two_per_sm = 108 * 1024;  // (228 KB - reserved - static) / 2
     if (P.persist_minb == 2 &&
         std::max<size_t>((size_t)pick_persist(nt, 2).smem, potrf_smem(nt, &in_smem) + xs_bytes) > two_per_sm)

@@ -14,6 +14,9 @@ CASE_NAMES = ["a64", "b200", "c500bd", "d1000", "e2000s", "f48", "g7", "h1"]
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
+    # a device hang must fail the test, not the GPU box (pytest-timeout)
+    if config.pluginmanager.hasplugin("timeout") and not config.getoption("timeout", None):
+        config.option.timeout = 600
 
 
 def load_case(name):
