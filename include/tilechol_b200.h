@@ -56,6 +56,11 @@ int tc_etree_fill_count(int64_t n, const int64_t* row_ptr, const int64_t* row_co
 
 /* reference ordering.py:239-263 symbolic_fill_count(m, p): nnz(L) incl. the
  * diagonal of P A P^T (forward may be NULL for the identity). */
+/* Zero-fill test of the identity ordering (parallel perfect-elimination
+ * check); *perfect = 1 iff nnz(L) = nnz(lower A), *offdiag = strictly lower
+ * entries.  Shortcut in front of tc_symbolic_fill_count for select_ordering
+ * (reference ordering.py:266-275: identity wins unless strictly beaten). */
+int tc_zero_fill(int64_t n, const int64_t* col_ptr, const int32_t* row_idx, int32_t* perfect, int64_t* offdiag);
 int tc_symbolic_fill_count(int64_t n, const int64_t* col_ptr, const int32_t* row_idx,
                            const int64_t* forward, int64_t* out_nnz_factor);
 

@@ -48,6 +48,7 @@ SIGNATURES = {
     "tc_device_count": (i32, []),
     "tc_etree_fill_count": (C.c_int, [i64, i64p, i64p, i64p]),
     "tc_symbolic_fill_count": (C.c_int, [i64, i64p, i32p, i64p, i64p]),
+    "tc_zero_fill": (C.c_int, [i64, i64p, i32p, i32p, i64p]),
     "tc_structure_stats": (C.c_int, [i64, i64p, i32p, f64, i64p, i64p]),
     "tc_factor_column_counts": (C.c_int, [i64, i64p, i32p, i64p, i64p]),
     "tc_arrowhead_pattern": (C.c_int, [i64, i64, i64, i32, i64p, i32p]),

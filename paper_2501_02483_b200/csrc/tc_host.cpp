@@ -18,6 +18,7 @@
 #include <memory>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "tilechol_b200.h"
@@ -363,6 +364,56 @@ extern "C" int tc_symbolic_fill_count(int64_t n, const int64_t* cp, const int32_
     std::vector<int64_t> rp, rc;
     lower_rows(n, cp, ri, fwd, rp, rc);
     *out = etree_count(n, rp.data(), rc.data()) + n;
+    return TC_OK;
+    GUARD_END
+}
+
+// Zero-fill test of the identity ordering, parallel over columns: the
+// elimination order is perfect (nnz(L) = nnz(lower A)) iff for every column
+// j the higher neighbours other than the lowest one, m(j), are neighbours of
+// m(j) (Rose-Tarjan-Lueker / Tarjan-Yannakakis perfect-elimination test).
+// *out = 1 and *offdiag = strictly-lower entries when perfect, else *out = 0.
+// Row indices are ascending within each column (canonical CSC).
+extern "C" int tc_zero_fill(int64_t n, const int64_t* cp, const int32_t* ri, int32_t* out, int64_t* offdiag) {
+    if (n < 1 || !cp || !ri || !out || !offdiag) return herr(TC_ERR_ARG, "zero_fill: bad arguments");
+    GUARD_BEGIN
+    const int nth = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    std::vector<int64_t> off(nth, 0);
+    std::vector<char> bad(nth, 0);
+    std::vector<std::thread> th;
+    const int64_t chunk = (n + nth - 1) / nth;
+    for (int w = 0; w < nth; ++w)
+        th.emplace_back([&, w]() {
+            const int64_t j0 = w * chunk, j1 = std::min<int64_t>(n, j0 + chunk);
+            int64_t cnt = 0;
+            for (int64_t j = j0; j < j1 && !bad[w]; ++j) {
+                int64_t p = cp[j];
+                const int64_t e = cp[j + 1];
+                while (p < e && ri[p] <= j) ++p;  // skip the diagonal (and any upper entry)
+                cnt += e - p;
+                if (e - p <= 1) continue;
+                const int64_t m = ri[p];
+                int64_t a = p + 1, b = cp[m];
+                const int64_t be = cp[m + 1];
+                for (; a < e; ++a) {  // rows of column j above m(j) must all be in column m(j)
+                    while (b < be && ri[b] < ri[a]) ++b;
+                    if (b == be || ri[b] != ri[a]) {
+                        bad[w] = 1;
+                        break;
+                    }
+                }
+            }
+            off[w] = cnt;
+        });
+    for (auto& t : th) t.join();
+    int64_t tot = 0;
+    bool ok = true;
+    for (int w = 0; w < nth; ++w) {
+        tot += off[w];
+        ok = ok && !bad[w];
+    }
+    *out = ok ? 1 : 0;
+    *offdiag = tot;
     return TC_OK;
     GUARD_END
 }

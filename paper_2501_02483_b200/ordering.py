@@ -171,7 +171,12 @@ def select_ordering(m: SymmetricCsc, candidates) -> Permutation:
     the reference's eager evaluation returns (e.g. BASELINE C1/C4, survey §8(a)
     row 8), without an RCM of a 2.5e9-entry pattern."""
     best = Permutation.identity(m.n)
-    best_nnz = symbolic_fill_count(m, None).nnz_factor
+    # parallel perfect-elimination test first: with zero fill the identity's
+    # nnz(L) is nnz(lower A) without the sequential elimination-tree pass
+    cp, ri = _csc(m)
+    perfect, offd = np.zeros(1, dtype=np.int32), np.zeros(1, dtype=np.int64)
+    check("tc_zero_fill", lib.tc_zero_fill(m.n, ptr(cp, i64p), ptr(ri, i32p), ptr(perfect, i32p), ptr(offd, i64p)))
+    best_nnz = int(offd[0]) + m.n if perfect[0] else symbolic_fill_count(m, None).nnz_factor
     for cand in candidates:
         if best_nnz <= m.nnz:
             break

@@ -204,3 +204,28 @@ def test_select_ordering_zero_fill_short_circuit():
         return ordering.Permutation.identity(m.n)
     p = ordering.select_ordering(m, [cand, cand])
     assert p.is_identity() and not called
+
+
+def test_zero_fill_shortcut_matches_etree_count():
+    """tc_zero_fill (parallel perfect-elimination test in front of the
+    sequential elimination-tree count, ordering.select_ordering) agrees with
+    the reference fill count: perfect <=> nnz(L) == nnz(lower A), and then
+    offdiag + n == nnz(L).  Band+arrow (zero fill), variable band (fill)."""
+    import numpy as np
+    from paper_2501_02483_b200 import matcore, ordering
+    from paper_2501_02483_b200._lib import lib, ptr, i64p, i32p
+    cases = [matcore.generate_arrowhead(matcore.ArrowheadSpec(3000, 60, 20, seed=1)),
+             matcore.generate_arrowhead(matcore.ArrowheadSpec(500, 7, 3, block_diagonal=True, seed=2))]
+    m = cases[0]
+    p = ordering.rcm(m, pinned_tail=0)
+    cases.append(matcore.permute_symmetric(m, p))  # scrambled: fill appears
+    for m in cases:
+        cp, ri = ordering._csc(m)
+        perfect, offd = np.zeros(1, dtype=np.int32), np.zeros(1, dtype=np.int64)
+        assert lib.tc_zero_fill(m.n, ptr(cp, i64p), ptr(ri, i32p), ptr(perfect, i32p), ptr(offd, i64p)) == 0
+        nnz_l = ordering.symbolic_fill_count(m, None).nnz_factor
+        assert bool(perfect[0]) == (nnz_l == int(offd[0]) + m.n)
+        if perfect[0]:
+            assert int(offd[0]) + m.n == nnz_l
+        else:
+            assert nnz_l > int(offd[0]) + m.n
