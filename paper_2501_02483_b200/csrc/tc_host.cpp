@@ -457,17 +457,42 @@ extern "C" int tc_structure_stats(int64_t n, const int64_t* cp, const int32_t* r
                                   int64_t* th) {
     if (n < 1 || !cp || !ri || !bw || !th) return herr(TC_ERR_ARG, "structure_stats: bad arguments");
     GUARD_BEGIN
+    // threads over column ranges: per-thread row histograms (summed), then
+    // per-thread bandwidth maxima (integer results, order-independent)
+    const int nth = cp[n] > (1 << 24) ? (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency())) : 1;
+    const int64_t chunk = (n + nth - 1) / nth;
+    std::vector<std::vector<int64_t>> part(nth);
+    auto run = [&](auto&& f) {
+        std::vector<std::thread> th;
+        for (int w = 0; w < nth; ++w) th.emplace_back(f, w);
+        for (auto& x : th) x.join();
+    };
+    run([&](int w) {
+        part[w].assign(n, 0);
+        const int64_t c0 = w * chunk, c1 = std::min<int64_t>(n, c0 + chunk);
+        for (int64_t e = cp[c0]; e < cp[c1]; ++e) part[w][ri[e]]++;
+    });
     std::vector<int64_t> cnt(n, 0);
-    for (int64_t e = 0; e < cp[n]; ++e) cnt[ri[e]]++;
+    for (int w = 0; w < nth; ++w) {
+        for (int64_t r = 0; r < n; ++r) cnt[r] += part[w][r];
+        std::vector<int64_t>().swap(part[w]);
+    }
     for (int64_t c = 0; c < n; ++c) cnt[c] += cp[c + 1] - cp[c] - 1;
     const double need = thr * (double)n;
     int64_t t = 0;
     while (t < n && (double)cnt[n - 1 - t] >= need) ++t;
     const int64_t nh = n - t;
+    std::vector<int64_t> bws(nth, 0);
+    run([&](int w) {
+        const int64_t c0 = w * chunk, c1 = std::min<int64_t>(n, c0 + chunk);
+        int64_t b = 0;
+        for (int64_t c = c0; c < c1; ++c)
+            for (int64_t e = cp[c]; e < cp[c + 1]; ++e)
+                if (ri[e] < nh) b = std::max<int64_t>(b, ri[e] - c);
+        bws[w] = b;
+    });
     int64_t b = 0;
-    for (int64_t c = 0; c < n; ++c)
-        for (int64_t e = cp[c]; e < cp[c + 1]; ++e)
-            if (ri[e] < nh) b = std::max<int64_t>(b, ri[e] - c);
+    for (int w = 0; w < nth; ++w) b = std::max(b, bws[w]);
     *bw = b;
     *th = t;
     return TC_OK;
@@ -617,8 +642,49 @@ extern "C" int tc_symbolic_from_csc(int64_t n, int32_t nt, const int64_t* cp, co
     if (T64 > INT32_MAX / 2) return herr(TC_ERR_ARG, "symbolic_from_csc: too many tiles");
     h->T = (int)T64;
     std::vector<std::vector<int32_t>> cols(h->T);
+    // canonical lower CSC: every entry of tile column tc lands in cols[tc],
+    // so tile columns are independent -> threads over tile-column ranges
+    // (same per-column order as the serial scan); any upper entry sends the
+    // whole scan to the serial path below
+    bool par_ok = cp[n] > (1 << 24);
+    if (par_ok) {
+        const int nth = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+        const int64_t tch = (h->T + nth - 1) / nth;
+        std::vector<char> upper(nth, 0), range(nth, 0);
+        std::vector<std::thread> th;
+        for (int w = 0; w < nth; ++w)
+            th.emplace_back([&, w]() {
+                std::vector<int32_t> mk(h->T, -1);
+                const int64_t t0 = w * tch, t1 = std::min<int64_t>(h->T, t0 + tch);
+                for (int64_t tc = t0; tc < t1; ++tc)
+                    for (int64_t c = tc * nt; c < std::min<int64_t>(n, (tc + 1) * nt); ++c)
+                        for (int64_t e = cp[c]; e < cp[c + 1]; ++e) {
+                            const int64_t r = ri[e];
+                            if (r < 0 || r >= n) {
+                                range[w] = 1;
+                                return;
+                            }
+                            if (r < c) {
+                                upper[w] = 1;
+                                return;
+                            }
+                            const int32_t tr = (int32_t)(r / nt);
+                            if (mk[tr] != (int32_t)tc) {
+                                mk[tr] = (int32_t)tc;
+                                cols[tc].push_back(tr);
+                            }
+                        }
+            });
+        for (auto& x : th) x.join();
+        for (int w = 0; w < nth; ++w) {
+            if (range[w]) return herr(TC_ERR_ARG, "symbolic_from_csc: row index out of range");
+            if (upper[w]) par_ok = false;
+        }
+        if (!par_ok)
+            for (auto& v : cols) v.clear();
+    }
     std::vector<int32_t> mark(h->T, -1);
-    for (int64_t c = 0; c < n; ++c) {
+    for (int64_t c = 0; c < n && !par_ok; ++c) {
         const int32_t tc = (int32_t)(c / nt);
         for (int64_t e = cp[c]; e < cp[c + 1]; ++e) {
             int64_t r = ri[e];
