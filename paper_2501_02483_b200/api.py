@@ -35,8 +35,6 @@ _ORDERINGS = ("auto", "identity", "partial-rcm", "min-degree", "adaptable-nd")
 _REDUCTIONS = ("auto", "on", "off")
 
 
-def _experimental_enabled() -> bool:
-    return os.environ.get("TILECHOL_EXPERIMENTAL", "") not in ("", "0")
 
 
 @dataclass(frozen=True)
@@ -52,10 +50,11 @@ class FactorOptions:
     changes the summation order, so "on"/"auto" factors agree with the
     sequential reference within rounding, not bitwise.
 
-    ``occupancy`` = 2 (two persistent CTAs per SM) and ``concurrent`` > 1
-    (grid-shared batch lanes) are experimental: they have shown rare
-    log-determinant drift and are rejected unless the
-    environment sets TILECHOL_EXPERIMENTAL=1."""
+    ``occupancy`` = 2 (two persistent CTAs per SM, 128-register cap) and
+    ``concurrent`` > 1 (grid-shared batch lanes) are supported: the round-1
+    race they exposed (a POTRF worker flag published before its rank-8
+    update) is fixed and tests/test_gpu_stress.py checks both
+    modes bitwise.  At nt = 128 one CTA per SM is the faster default."""
 
     tile_size: int = 120
     workers: int = 1
@@ -64,7 +63,7 @@ class FactorOptions:
     lookahead: int = 3             # bulk-update lookahead depth in columns (0/False = off)
     executor: str = "persistent"  # persistent | graph | direct
     chunk: int = 0
-    occupancy: int = 0             # persistent CTAs per SM (0 = 1; 2 = experimental)
+    occupancy: int = 0             # persistent CTAs per SM (0 = 1 CTA/SM; 2 = two per SM, 128-register cap)
     concurrent: int = 1            # factorisations meant to share the GPU (batch lanes)
 
     def __post_init__(self):
@@ -82,9 +81,7 @@ class FactorOptions:
             raise ValueError(f"occupancy must be 0, 1 or 2, got {self.occupancy}")
         if self.concurrent < 1:
             raise ValueError(f"concurrent must be >= 1, got {self.concurrent}")
-        if (self.occupancy == 2 or self.concurrent > 1) and not _experimental_enabled():
-            raise ValueError("occupancy=2 / concurrent>1 are experimental (rare log-determinant drift, "
-                             "DESIGN.md §10); set TILECHOL_EXPERIMENTAL=1 to enable them")
+
 
     def plan_options(self) -> PlanOptions:
         W = self.workers if self.workers >= 2 else 8

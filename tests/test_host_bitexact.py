@@ -176,20 +176,17 @@ def test_inla_lincomb_is_bitwise_values():
         assert np.array_equal(v, fam.values(*th))
 
 
-def test_experimental_modes_are_gated(monkeypatch):
-    """occupancy=2 / concurrent>1 showed rare logdet drift:
-    rejected unless TILECHOL_EXPERIMENTAL=1."""
+def test_occupancy_and_concurrency_options_validated():
+    """occupancy 1/2 and concurrent >= 1 are accepted (the round-1 race is
+    fixed); anything else is rejected."""
     import pytest
     from paper_2501_02483_b200.api import FactorOptions
-    monkeypatch.delenv("TILECHOL_EXPERIMENTAL", raising=False)
     FactorOptions(occupancy=1, concurrent=1)
-    for kw in ({"occupancy": 2}, {"concurrent": 2}):
-        with pytest.raises(ValueError, match="experimental"):
-            FactorOptions(**kw)
+    FactorOptions(occupancy=2, concurrent=4)
     with pytest.raises(ValueError):
         FactorOptions(occupancy=3)
-    monkeypatch.setenv("TILECHOL_EXPERIMENTAL", "1")
-    FactorOptions(occupancy=2, concurrent=4)
+    with pytest.raises(ValueError):
+        FactorOptions(concurrent=0)
 
 
 def test_select_ordering_zero_fill_short_circuit():
