@@ -18,7 +18,7 @@
 // k_persist variants are instantiated in tc_persist_inst.cu (parallel build)
 namespace tc {
 #define TC_EXTERN(G, BM, BN, WGM, WGN, KS, MINB, SB) \
-    extern template __global__ void k_persist<BM, BN, WGM, WGN, KS, MINB, SB>(PersistArgs);
+    extern template __global__ void k_persist<BM, BN, WGM, WGN, KS, MINB, SB>(const __grid_constant__ PersistArgs);
 TC_PERSIST_VARIANTS(TC_EXTERN)
 #undef TC_EXTERN
 }  // namespace tc
@@ -123,12 +123,14 @@ UpdKernel pick_upd_small(int nt) {
 struct PersistKernel {
     void (*fn)(PersistArgs);
     int BM, BN, smem;
+    int lda, ldb, kc;  // update operand staging: padded column strides, k-chunk (TMA boxes)
 };
 
 template <int BM, int BN, int WGM, int WGN, int KS, int SB>
 PersistKernel mk_persist_sb(int minb) {
+    using U = UpdCfg<BM, BN, WGM, WGN, KS>;
     return PersistKernel{minb == 2 ? k_persist<BM, BN, WGM, WGN, KS, 2, SB> : k_persist<BM, BN, WGM, WGN, KS, 1, SB>,
-                         BM, BN, UpdCfg<BM, BN, WGM, WGN, KS>::SMEM};
+                         BM, BN, U::SMEM, U::LDA, U::LDB, U::KC};
 }
 // Only the small-block variants a shape can meet are instantiated (compile
 // time): small_block(nt) for the tile sizes that select each update shape.
@@ -148,7 +150,8 @@ PersistKernel mk_persist(int minb, int nt) {
 // minb = minimum resident CTAs per SM the variant is compiled for
 template <int BM, int BN, int WGM, int WGN, int KS, int SB>
 PersistKernel mk_persist1() {
-    return PersistKernel{k_persist<BM, BN, WGM, WGN, KS, 1, SB>, BM, BN, UpdCfg<BM, BN, WGM, WGN, KS>::SMEM};
+    using U = UpdCfg<BM, BN, WGM, WGN, KS>;
+    return PersistKernel{k_persist<BM, BN, WGM, WGN, KS, 1, SB>, BM, BN, U::SMEM, U::LDA, U::LDB, U::KC};
 }
 PersistKernel pick_persist(int nt, int minb) {
     if (small_block(nt) == 32) {
@@ -641,6 +644,7 @@ struct tc_plan {
     int persist_trsm_ring = 0;  // 0 = auto staging, >0 = strip ring of that many buffers
     int persist_minb = 2;
     int persist_trsm_rows = 64;  // TRSM strip rows of the persistent executor
+    bool persist_tma = false;    // update operands through TMA tensor maps
     int persist_grid = 0;
     // fused diagonal SYRK: POTRF(k) applies the last update of its diagonal
     // tile itself, consuming L(k, n_last) panel by panel from TRSM(n_last)
@@ -1263,6 +1267,8 @@ int build_persistent(tc_plan& P) {
     // DESIGN.md §10) that one CTA per SM has not shown; opt-in until found.
     const int occ_mode = P.opts.reserved[1];
     P.persist_minb = occ_mode == 2 && !big_shape(nt) ? 2 : 1;
+    // TMA operand staging needs 16-byte row strides (nt even); TC_UPD_TMA=0 turns it off
+    P.persist_tma = (nt % 2 == 0) && !(getenv("TC_UPD_TMA") && atoi(getenv("TC_UPD_TMA")) == 0);
     bool in_smem;
     // shared memory: the max over task kinds; the fused TRSM may stage L
     // strip by strip (ring) instead of whole when that lets two CTAs share an SM
@@ -1301,6 +1307,30 @@ int build_persistent(tc_plan& P) {
     const int conc = std::max(1, (int)P.opts.reserved[2]);
     P.persist_grid = std::max(1, (per_sm * sms) / conc);
     CK(cudaStreamSynchronize(s0));
+    return TC_OK;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+int encode_tile_map(CUtensorMap* m, double* storage, int nt, int64_t S, int box_rows, int box_k) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+        if (!f || q != cudaDriverEntryPointSuccess) return set_err(TC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = (EncodeTiledFn)f;
+    }
+    const cuuint64_t dims[3] = {(cuuint64_t)nt, (cuuint64_t)nt, (cuuint64_t)S};
+    const cuuint64_t strides[2] = {(cuuint64_t)nt * 8, (cuuint64_t)nt * nt * 8};
+    const cuuint32_t box[3] = {(cuuint32_t)box_rows, (cuuint32_t)box_k, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, storage, dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(TC_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return TC_OK;
 }
 
@@ -1343,6 +1373,15 @@ int run_persistent(tc_plan& P, Lane& ln, cudaStream_t s) {
     a.xper = ((P.nt + P.persist_trsm_rows - 1) / P.persist_trsm_rows) * (P.persist_trsm_rows / 8);
     a.trsm_rows = P.persist_trsm_rows;
     const PersistKernel K = pick_persist(P.nt, P.persist_minb);
+    a.use_tma = 0;
+    if (P.persist_tma) {
+        // TMA descriptors of this storage: a 3-D tensor [S][nt][nt] (rows
+        // innermost), boxes = the update kernel's padded stage layout
+        const int r1 = encode_tile_map(&a.tmA, ln.h.storage, P.nt, P.S, K.lda, K.kc);
+        const int r2 = r1 ? r1 : encode_tile_map(&a.tmB, ln.h.storage, P.nt, P.S, K.ldb, K.kc);
+        if (r2) return r2;
+        a.use_tma = 1;
+    }
     K.fn<<<P.persist_grid, kPersistThreads, P.persist_smem, s>>>(a);
     CK(cudaGetLastError());
     return TC_OK;

@@ -6,7 +6,7 @@
 namespace tc {
 #define TC_INST(G, BM, BN, WGM, WGN, KS, MINB, SB) \
     TC_INST_##G(BM, BN, WGM, WGN, KS, MINB, SB)
-#define TC_DO(BM, BN, WGM, WGN, KS, MINB, SB) template __global__ void k_persist<BM, BN, WGM, WGN, KS, MINB, SB>(PersistArgs);
+#define TC_DO(BM, BN, WGM, WGN, KS, MINB, SB) template __global__ void k_persist<BM, BN, WGM, WGN, KS, MINB, SB>(const __grid_constant__ PersistArgs);
 #define TC_SKIP(BM, BN, WGM, WGN, KS, MINB, SB)
 #if TC_INST_GROUP == 0
 #define TC_INST_0 TC_DO
