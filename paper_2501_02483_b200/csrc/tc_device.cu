@@ -644,6 +644,7 @@ struct tc_plan {
     int persist_trsm_ring = 0;  // 0 = auto staging, >0 = strip ring of that many buffers
     int persist_minb = 2;
     int persist_trsm_rows = 64;  // TRSM strip rows of the persistent executor
+    PersistKernel pkern{};       // the persistent kernel variant chosen at plan time
     bool persist_tma = false;    // update operands through TMA tensor maps
     int persist_grid = 0;
     // fused diagonal SYRK: POTRF(k) applies the last update of its diagonal
@@ -1279,6 +1280,7 @@ int build_persistent(tc_plan& P) {
         P.persist_minb = 1;  // two CTAs cannot share an SM (packed POTRF tile too large): no register cap
     const PersistKernel K = pick_persist(nt, P.persist_minb);
     if (!K.fn) return set_err(TC_ERR_ARG, "plan: no persistent kernel variant for tile size %d", nt);
+    P.pkern = K;  // fixed at plan time (the selection reads tuning environment variables)
     const size_t base = std::max<size_t>({(size_t)K.smem, potrf_smem(nt, &in_smem) + xs_bytes, (size_t)4096});
     const int TR = P.persist_trsm_rows;
     const size_t t_full = trsm_smem_rows(TR, nt);
@@ -1372,7 +1374,7 @@ int run_persistent(tc_plan& P, Lane& ln, cudaStream_t s) {
     a.xctr_of_slot = P.d_xctr_of_slot;
     a.xper = ((P.nt + P.persist_trsm_rows - 1) / P.persist_trsm_rows) * (P.persist_trsm_rows / 8);
     a.trsm_rows = P.persist_trsm_rows;
-    const PersistKernel K = pick_persist(P.nt, P.persist_minb);
+    const PersistKernel& K = P.pkern;
     a.use_tma = 0;
     if (P.persist_tma) {
         // TMA descriptors of this storage: a 3-D tensor [S][nt][nt] (rows

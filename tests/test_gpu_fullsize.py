@@ -118,3 +118,34 @@ def test_c4_full_arrowhead(torch):
     be = bench.device_backward_error(pat, m, st, vals, offs, sh)
     assert be["backward_error"] <= BACKWARD_TOL, be
     _prefix_check("c4", 128, pat, st, 2e11)
+
+
+@pytest.mark.parametrize("shape", [None, "128x64"])
+def test_arrowhead_logdet_independent_of_tile_size(torch, monkeypatch, shape):
+    """A mid-size band + arrow matrix (n=60,000, b=1000, t=300: wide columns
+    and long arrow chains like C4) factorised at every update block shape the
+    tile sizes select (40x40 @120, 64x64 @128, 80x40 @160, 80x48 @240, 64x64
+    @256, 128x64 on request) gives the oracle's log-determinant; catches a
+    wrong operand staging path that only wide-column plans exercise."""
+    import oracle as O
+    from paper_2501_02483_b200 import api, matcore
+    if shape:
+        monkeypatch.setenv("TC_UPD_SHAPE", shape)
+    m = matcore.generate_arrowhead(matcore.ArrowheadSpec(60_000, 1000, 300, seed=4))
+    d = m.values[m.col_ptr[:-1]]
+    ref = None
+    for nt in ([128] if shape else [120, 128, 160, 240, 256]):
+        ld = api.logdet(api.factorize(m, api.FactorOptions(tile_size=nt, ordering="identity")))
+        if ref is None:
+            # oracle: the reference op stream at nt=120 through oracle.run_ops
+            import bench  # noqa: F401  (repo root on sys.path)
+            from paper_2501_02483_b200 import ctsf, symbolic
+            g = ctsf.build_tile_grid(m, 120)
+            sy = symbolic.tile_symbolic_factorize(g)
+            op, dst, s1, s2 = symbolic.compile_ops(sy)[:4]
+            st = ctsf.pack_into_grid(m, sy.factor_grid).storage
+            p, info = O.run_ops(st, np.zeros((0, 120, 120)), op, dst, s1, s2, 0, op.size)
+            assert info == -1
+            ref = O.logdet(st, sy.factor_grid.slot_map, m.n, 120)
+        assert abs(ld - ref) <= 1e-10 * abs(ref), (nt, ld, ref)
+    assert np.all(d > 0)
