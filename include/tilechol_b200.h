@@ -170,7 +170,7 @@ typedef struct tc_plan_opts {
     int32_t tree_workers;   /* W partial accumulators per long chain; 0 = 8 */
     int32_t tree_threshold; /* chains with accum >= threshold are split; 0 = 2*W, <0 = off */
     int32_t chunk;          /* columns per split-K chunk launch; 0 = auto */
-    int32_t lookahead;      /* D >= 1: last D contributing columns split off the bulk update; 0 = off */
+    int32_t lookahead;      /* D >= 1: last D contributing columns split off the bulk update; 0 = off; < 0 = auto (3 / 4) */
     int32_t use_graph;      /* 2 = persistent (default), 1 = CUDA graph, 0 = direct launches */
     int32_t reserved[3];    /* [0] 1 = no POTRF->TRSM streaming, [1] persistent CTAs/SM (0 auto),
                                [2] concurrent factorisations sharing the GPU (grid share) */

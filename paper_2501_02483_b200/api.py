@@ -60,7 +60,7 @@ class FactorOptions:
     workers: int = 1
     ordering: str = "auto"
     tree_reduction: str = "auto"
-    lookahead: int = 3             # bulk-update lookahead depth in columns (0/False = off)
+    lookahead: int = -1            # bulk-update lookahead depth in columns (-1 = auto: 3 wide / 4 narrow columns; 0/False = off)
     executor: str = "persistent"  # persistent | graph | direct
     chunk: int = 0
     occupancy: int = 0             # persistent CTAs per SM (0 = 1 CTA/SM; 2 = two per SM, 128-register cap)

@@ -37,7 +37,7 @@ class PlanOptions:
     tree_workers: int = 8        # W partial accumulators per long chain
     tree_threshold: int = 0      # 0 = 2*W (reference rule), < 0 = no tree reduction
     chunk: int = 0               # columns per split-K launch (0 = 8)
-    lookahead: int = 3           # columns of lookahead for the bulk update (0 = off)
+    lookahead: int = -1          # columns of lookahead for the bulk update (-1 = auto, 0 = off)
     executor: str = "persistent"  # persistent | graph | direct
     occupancy: int = 0            # persistent CTAs per SM: 0 auto (2 when it fits), 1, 2
     fuse_trsm: bool = True        # persistent: TRSM(k) streams POTRF(k)'s panels
