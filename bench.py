@@ -670,7 +670,7 @@ def run_ours(a, name, nt, rank, world):
             "data": "synthetic", "config": common_config(name, nt, world, a),
             "structure": {"nnz": m.nnz, "tiles_per_side": T, "slots": S, "tile_storage_gb": B / 2 / 1e9,
                           "executor": a.executor,
-                          "lookahead": opts.lookahead if opts.lookahead >= 0 else (3 if plan.S >= 16 * plan.T else 4)},
+                          "lookahead": opts.lookahead if opts.lookahead >= 0 else (3 if plan.S >= 20 * plan.T else 4)},
             "time_to_factor_ms": ms, "gflops_tile": F / (ms * 1e-3) / 1e9,
             "gflops_useful": useful / (ms * 1e-3) / 1e9 if useful else None,
             "fp64_roofline": {"time_ms": t_roof * 1e3, "frac": t_roof * 1e3 / ms, "tile_flops": F,

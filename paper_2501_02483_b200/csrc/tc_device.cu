@@ -679,10 +679,10 @@ int build_plan(tc_plan& P) {
         P.cs[P.fcol[s] + 1]++;
     }
     for (int k = 0; k < T; ++k) P.cs[k + 1] += P.cs[k];
-    // lookahead < 0: automatic -- 3 on wide-column plans (>= 16 tiles per
-    // column on average, e.g. C4: 480 vs 505 ms at 4), 4 otherwise (C3 @128:
-    // 77 vs 86 ms at 3)
-    if (P.opts.lookahead < 0) P.opts.lookahead = S >= 16 * (int64_t)T ? 3 : 4;
+    // lookahead < 0: automatic -- 3 on wide-column plans (>= 20 tiles per
+    // column on average, e.g. C4 @128 with 22: 480 vs 507 ms at 4), 4
+    // otherwise (C3 @128 with 18.8: 77 vs 87 ms at 3)
+    if (P.opts.lookahead < 0) P.opts.lookahead = S >= 20 * (int64_t)T ? 3 : 4;
     for (int k = 0; k < T; ++k)
         if (P.cs[k + 1] == P.cs[k] || P.frow[P.cs[k]] != k)
             return set_err(TC_ERR_ARG, "plan: diagonal tile %d missing", k);
