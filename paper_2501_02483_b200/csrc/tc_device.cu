@@ -185,7 +185,7 @@ size_t potrf_smem(int nt, bool* in_smem) {
         return packed;
     }
     *in_smem = false;
-    return (size_t)ntp * 8;
+    return potrf_smem_bytes(ntp, false);  // two-level path (nt <= 256) or 1/diag only
 }
 
 bool potrf_supported(int nt) {
