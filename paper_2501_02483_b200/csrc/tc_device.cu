@@ -177,9 +177,20 @@ int prep_kernel(const void* fn, int smem) {
 }
 
 // packed lower block rows in shared memory up to ntp = 184, else in place
+// smallest tile size factored by the two-level POTRF (TC_POTRF2_MIN; default:
+// only tiles whose packed triangle does not fit shared memory)
+int potrf2_min() {
+    static const int v = getenv("TC_POTRF2_MIN") ? atoi(getenv("TC_POTRF2_MIN")) : 185;
+    return v;
+}
+
 size_t potrf_smem(int nt, bool* in_smem) {
     const int ntp = (nt + 7) & ~7;
     const size_t packed = potrf_packed_doubles(ntp) * 8 + (size_t)ntp * 8;
+    if (nt % 8 == 0 && nt >= 16 && nt <= 256 && nt >= potrf2_min()) {
+        *in_smem = false;
+        return potrf_smem_bytes(ntp, false);
+    }
     if (packed <= 218 * 1024) {
         *in_smem = true;
         return packed;
@@ -564,6 +575,8 @@ namespace {
 
 enum LaunchKind { L_UPD = 0, L_POTRF = 1, L_TRSM = 2, L_COMBINE = 3, L_LOGDET = 4 };
 
+// trace classification of a launch (tc_plan_trace launch_meta bits 8..10)
+constexpr int kTagChain = 1 << 8, kTagMid = 1 << 9, kTagSub = 1 << 10;
 struct Launch {
     int kind = 0;
     int high = 0;                // critical-path priority
@@ -574,6 +587,7 @@ struct Launch {
     uint32_t live = 0;           // COMBINE
     int cls = 0;                 // profiling class: 0 bulk, 1 last, 2 potrf, 3 trsm, 4 combine, 5 logdet, 6 split-K chunk
     int small = 0;               // UPD items use the small latency block (L(k) launches)
+    int tag = 0;                 // trace classification bits (kTag*)
     double flops = 0.0;          // algorithmic flops of this launch
     std::vector<int32_t> deps;
 };
@@ -628,7 +642,7 @@ struct tc_plan {
     int prio_hi = 0, prio_lo = 0;
     int dev = 0;
     // per-column launch ids (persistent ticket order)
-    std::vector<int32_t> colB, colM, colL, colLo, colPot, colTrsm;
+    std::vector<int32_t> colB, colBd, colM, colMd, colL, colLc, colLo, colPot, colTrsm, colTrsmC;
     std::vector<std::vector<int32_t>> colComb, colChunk;
     // persistent executor
     std::vector<PTask> ptasks;
@@ -665,6 +679,22 @@ int64_t find_slot(const tc_plan& P, int32_t m, int32_t c) {
 }
 
 int build_persistent(tc_plan& P);
+
+// TC_CRIT=0: one L_off(k) / TRSM(k) launch for every off-diagonal target
+static bool crit_split() {
+    static const bool v = !(getenv("TC_CRIT") && atoi(getenv("TC_CRIT")) == 0);
+    return v;
+}
+// TC_BSPLIT=0: one bulk-update launch B(k) per column (diagonal tile included)
+static bool b_split() {
+    static const bool v = !(getenv("TC_BSPLIT") && atoi(getenv("TC_BSPLIT")) == 0);
+    return v;
+}
+// TC_MSPLIT=0: one near-update launch M(k) per column (diagonal tile included)
+static bool m_split() {
+    static const bool v = !(getenv("TC_MSPLIT") && atoi(getenv("TC_MSPLIT")) == 0);
+    return v;
+}
 
 int build_plan(tc_plan& P) {
     const int T = P.T, nt = P.nt;
@@ -764,15 +794,20 @@ int build_plan(tc_plan& P) {
     P.launches.clear();
     P.colB.assign(T, -1);
     P.colM.assign(T, -1);
+    P.colMd.assign(T, -1);
+    P.colBd.assign(T, -1);
     P.colL.assign(T, -1);
     P.colLo.assign(T, -1);
     P.colPot.assign(T, -1);
     P.colTrsm.assign(T, -1);
+    P.colTrsmC.assign(T, -1);
+    P.colLc.assign(T, -1);
     P.colComb.assign(T, {});
     P.colChunk.assign(T, {});
     P.items.clear();
     P.tgts.clear();
     std::vector<int32_t> pnode(T, -1);           // launch finishing column k
+    std::vector<int32_t> pcrit(T, -1);           // TRSMc(k) when column k's TRSM is split
     std::vector<uint32_t> live_mask(S, 0);
     std::vector<std::vector<int32_t>> buf_writer(S);  // per reduced target: last chunk launch per residue
     const double n3 = (double)nt * nt * nt;
@@ -784,6 +819,7 @@ int build_plan(tc_plan& P) {
             const int32_t pa = parent[c];
             if (pa >= 0 && std::binary_search(cols.begin(), cols.end(), pa)) continue;
             deps.push_back(pnode[c]);
+            if (pcrit[c] >= 0) deps.push_back(pcrit[c]);
         }
     };
 
@@ -816,9 +852,16 @@ int build_plan(tc_plan& P) {
             while (x > tp0[t] && P.fcol[P.pairs[x - 1].b] >= col) --x;
             return x;
         };
-        // B(k): bulk pairs of non-reduced targets
-        int32_t bnode = -1, lnode = -1, mnode = -1;
-        {
+        // B(k): bulk pairs of non-reduced targets.  With the B split the
+        // diagonal tile's bulk pairs form their own launch Bd(k): the chain
+        // Bd(k) -> Md(k) -> L_diag(k) -> POTRF(k) then never waits for the
+        // column's long off-diagonal bulk items (C4: B(k+1) ended ~28 us into
+        // POTRF(k) and held Md(k+1) back)
+        int32_t bnode = -1, bdnode = -1, lnode = -1, mnode = -1;
+        const bool bsplit = SBK && m_split() && b_split();
+        for (int part = 0; part < 2; ++part) {
+            const bool dpart = part == 0;
+            if (dpart && !bsplit) continue;
             Launch L;
             L.kind = L_UPD;
             L.k = k;
@@ -826,6 +869,7 @@ int build_plan(tc_plan& P) {
             std::vector<int32_t> cols;
             for (int64_t t = c0; t < c1; ++t) {
                 if (red_base[t] >= 0) continue;
+                if (bsplit && ((t == c0) != dpart)) continue;
                 const int64_t p1 = cut(t, bcut);
                 if (p1 > tp0[t]) {
                     emit_items(t, tp0[t], p1, (int32_t)t, MODE_SUB);
@@ -836,19 +880,36 @@ int build_plan(tc_plan& P) {
             L.cnt = (int64_t)P.items.size() - L.off;
             if (L.cnt > 0) {
                 add_panel_deps(L.deps, cols);
-                bnode = (int32_t)P.launches.size();
-                P.colB[k] = bnode;
+                const int32_t id = (int32_t)P.launches.size();
+                if (dpart) {
+                    bdnode = id;
+                    P.colBd[k] = id;
+                } else {
+                    bnode = id;
+                    P.colB[k] = id;
+                }
                 P.launches.push_back(std::move(L));
             }
         }
-        if (nmid >= 0) {
+        // writers of the diagonal tile before Md(k) / of the rest before M(k)
+        const int32_t bprev_d = bsplit ? bdnode : bnode;
+        // M(k): with the L split, the diagonal tile's near pairs form their
+        // own launch Md(k) -- L_diag(k) and POTRF(k) wait only on it, so the
+        // chain no longer waits for the whole column's near update to get
+        // CTAs (C4 @128: M(k+1) ended ~7 us after TRSM(k), delaying L_diag)
+        int32_t mdnode = -1;
+        const bool msplit = SBK && m_split();
+        for (int part = 0; part < (msplit ? 2 : 1) && nmid >= 0; ++part) {
+            const bool dpart = msplit && part == 0;
             Launch L;
             L.kind = L_UPD;
             L.k = k;
+            L.tag = kTagMid;
             L.off = (int64_t)P.items.size();
             std::vector<int32_t> cols;
             for (int64_t t = c0; t < c1; ++t) {
                 if (red_base[t] >= 0) continue;
+                if (msplit && ((t == c0) != dpart)) continue;
                 const int64_t p0 = cut(t, nmid), p1 = cut(t, nlast);
                 if (p1 > p0) {
                     emit_items(t, p0, p1, (int32_t)t, MODE_SUB);
@@ -859,33 +920,55 @@ int build_plan(tc_plan& P) {
             L.cnt = (int64_t)P.items.size() - L.off;
             if (L.cnt > 0) {
                 add_panel_deps(L.deps, cols);
-                if (bnode >= 0) L.deps.push_back(bnode);
-                mnode = (int32_t)P.launches.size();
-                P.colM[k] = mnode;
+                const int32_t bp = dpart ? bprev_d : bnode;
+                if (bp >= 0) L.deps.push_back(bp);
+                if (!msplit && bdnode >= 0) L.deps.push_back(bdnode);
+                const int32_t id = (int32_t)P.launches.size();
+                if (dpart) {
+                    mdnode = id;
+                    P.colMd[k] = id;
+                } else {
+                    mnode = id;
+                    P.colM[k] = id;
+                }
                 P.launches.push_back(std::move(L));
             }
         }
-        const int32_t prev = mnode >= 0 ? mnode : bnode;  // last writer of column k before L(k)
+        // last writers of column k before L(k): the diagonal tile / the rest
+        const int32_t prev_d = msplit ? (mdnode >= 0 ? mdnode : bprev_d) : (mnode >= 0 ? mnode : bnode);
+        const int32_t prev = mnode >= 0 ? mnode : bnode;
         // L(k): the last contribution.  With small blocks available it is split
         // into L_diag(k) (the diagonal tile, small blocks: POTRF(k) waits only
         // on it) and L_off(k) (off-diagonal targets, regular blocks: only
         // TRSM(k) waits on them, and TRSM streams behind POTRF anyway)
-        int32_t lnode_off = -1;
+        // With the critical split (crit_split()) the first off-diagonal
+        // target c0+1 gets its own small-block launch L_crit(k) and its own
+        // TRSM launch TRSMc(k): the column chain POTRF(k) -> TRSMc(k) ->
+        // L_diag(k+1) no longer waits for the whole column's L_off(k).
+        int32_t lnode_off = -1, lnode_crit = -1;
+        const bool csplit = SBK && crit_split() && c1 - c0 > 1;
+        // L(k) items read tiles of column nlast only: the diagonal part reads
+        // (k, nlast), which TRSMc(nlast) alone produces when row k is column
+        // nlast's first off-diagonal row
+        const bool dcrit = nlast >= 0 && pcrit[nlast] >= 0 && P.frow[P.cs[nlast] + 1] == k;
         if (nlast >= 0) {
-            for (int part = 0; part < 2; ++part) {
-                const bool diag_part = part == 0;
+            for (int part = 0; part < 3; ++part) {
+                const bool diag_part = part == 0, crit_part = part == 1;
                 if (!SBK && !diag_part) break;  // unsplit: one launch, regular blocks
+                if (crit_part && !csplit) continue;
                 Launch L;
                 L.kind = L_UPD;
                 L.k = k;
                 L.high = 1;
                 L.cls = 1;
+                L.tag = diag_part ? kTagChain : (crit_part ? kTagChain | kTagSub : 0);
                 L.off = (int64_t)P.items.size();
-                small_now = SBK != 0 && diag_part;
+                small_now = SBK != 0 && (diag_part || crit_part);
                 L.small = small_now ? 1 : 0;
                 for (int64_t t = c0; t < c1; ++t) {
                     if (red_base[t] >= 0) continue;
                     if (SBK && ((t == c0) != diag_part)) continue;
+                    if (csplit && !diag_part && ((t == c0 + 1) != crit_part)) continue;
                     const int64_t p1 = tp1[t];
                     if (p1 > tp0[t] && P.fcol[P.pairs[p1 - 1].b] == nlast) {
                         emit_items(t, p1 - 1, p1, (int32_t)t, MODE_SUB);
@@ -895,12 +978,22 @@ int build_plan(tc_plan& P) {
                 small_now = false;
                 L.cnt = (int64_t)P.items.size() - L.off;
                 if (L.cnt > 0) {
-                    L.deps.push_back(pnode[nlast]);
-                    if (prev >= 0) L.deps.push_back(prev);
+                    if (diag_part && dcrit) {
+                        L.deps.push_back(pcrit[nlast]);
+                    } else {
+                        L.deps.push_back(pnode[nlast]);
+                        if (pcrit[nlast] >= 0) L.deps.push_back(pcrit[nlast]);
+                    }
+                    const int32_t pv = diag_part && SBK ? prev_d : prev;
+                    if (pv >= 0) L.deps.push_back(pv);
+                    if (!SBK && mdnode >= 0) L.deps.push_back(mdnode);
                     const int32_t id = (int32_t)P.launches.size();
                     if (diag_part) {
                         lnode = id;
                         P.colL[k] = id;
+                    } else if (crit_part) {
+                        lnode_crit = id;
+                        P.colLc[k] = id;
                     } else {
                         lnode_off = id;
                         P.colLo[k] = id;
@@ -936,8 +1029,13 @@ int build_plan(tc_plan& P) {
             L.cls = 2;
             L.k = k;
             L.slot = c0;
-            if (bnode >= 0) L.deps.push_back(bnode);
-            if (mnode >= 0) L.deps.push_back(mnode);
+            if (bsplit) {
+                if (bdnode >= 0) L.deps.push_back(bdnode);
+            } else if (bnode >= 0) {
+                L.deps.push_back(bnode);
+            }
+            if (mdnode >= 0) L.deps.push_back(mdnode);
+            if (mnode >= 0 && !msplit) L.deps.push_back(mnode);
             if (lnode >= 0) L.deps.push_back(lnode);
             for (int32_t x : comb_diag) L.deps.push_back(x);
             L.flops += n3 / 3.0;
@@ -946,25 +1044,50 @@ int build_plan(tc_plan& P) {
             P.launches.push_back(std::move(L));
         }
         pnode[k] = pot;
-        if (c1 - c0 > 1) {
+        for (int part = 0; part < 2; ++part) {
+            // part 0: TRSMc(k) (target c0+1 only, with the critical split) or
+            // the whole TRSM(k); part 1: TRSMr(k), the remaining targets
+            const int64_t t0 = (part == 0) ? c0 + 1 : c0 + 2;
+            const int64_t t1 = (part == 0 && csplit) ? std::min<int64_t>(c0 + 2, c1) : c1;
+            if ((part == 1 && !csplit) || t1 <= t0) continue;
             Launch L;
             L.kind = L_TRSM;
             L.high = 1;
             L.cls = 3;
             L.k = k;
             L.slot = c0;
+            L.tag = (csplit && part == 0) ? kTagChain : 0;
             L.off = (int64_t)P.tgts.size();
-            for (int64_t t = c0 + 1; t < c1; ++t) P.tgts.push_back((int32_t)t);
-            L.cnt = c1 - c0 - 1;
+            for (int64_t t = t0; t < t1; ++t) P.tgts.push_back((int32_t)t);
+            L.cnt = t1 - t0;
             L.deps.push_back(pot);
             if (bnode >= 0) L.deps.push_back(bnode);
+            if (bdnode >= 0) L.deps.push_back(bdnode);
             if (mnode >= 0) L.deps.push_back(mnode);
+            if (mdnode >= 0) L.deps.push_back(mdnode);
             if (lnode >= 0) L.deps.push_back(lnode);
-            if (lnode_off >= 0) L.deps.push_back(lnode_off);
+            if (csplit && part == 0) {
+                if (lnode_crit >= 0) L.deps.push_back(lnode_crit);
+            } else if (lnode_off >= 0) {
+                L.deps.push_back(lnode_off);
+            }
+            if (!csplit && lnode_crit >= 0) L.deps.push_back(lnode_crit);
             for (int32_t x : comb_off) L.deps.push_back(x);
-            L.flops += n3 * (double)(c1 - c0 - 1);
-            pnode[k] = (int32_t)P.launches.size();
-            P.colTrsm[k] = pnode[k];
+            L.flops += n3 * (double)(t1 - t0);
+            const int32_t id = (int32_t)P.launches.size();
+            if (csplit && part == 0) {
+                pcrit[k] = id;
+                P.colTrsmC[k] = id;
+                if (c1 - c0 == 2) {  // no other target: TRSMc finishes column k
+                    pnode[k] = id;
+                    pcrit[k] = -1;
+                    P.colTrsm[k] = id;
+                    P.colTrsmC[k] = -1;
+                }
+            } else {
+                pnode[k] = id;
+                P.colTrsm[k] = id;
+            }
             P.launches.push_back(std::move(L));
         }
         // split-K pieces of reduced chains that became ready with column k
@@ -1130,30 +1253,48 @@ int build_persistent(tc_plan& P) {
         pd.erase(std::remove_if(pd.begin(), pd.end(), [&](int32_t d) { return dead[d] != 0; }), pd.end());
     }
     const int D = std::max(1, P.opts.lookahead);
-    for (int j = 0; j < std::min(D, T); ++j) put(P.colB[j]);
+    for (int j = 0; j < std::min(D, T); ++j) {
+        put(P.colBd[j]);
+        put(P.colB[j]);
+    }
     // TC_ORDER=1: the next column's chain (M, L_diag, combines, POTRF) is
     // ticketed right behind this column's TRSM, ahead of the bulk update, so
     // it never waits for the bulk tickets to be handed out
     // default on for wide columns (>= 16 tiles per column on average, e.g.
     // C4: 536 -> 520 ms at nt=128), off for narrow ones (C3: 89 vs 97 ms)
     const bool chain_first = getenv("TC_ORDER") ? atoi(getenv("TC_ORDER")) == 1 : P.S >= 16 * (int64_t)T;
+    const bool md_early = !(getenv("TC_MD_EARLY") && atoi(getenv("TC_MD_EARLY")) == 0) && D >= 2;
     for (int k = 0; k < T; ++k) {
+        put(P.colMd[k]);
         put(P.colM[k]);
         put(P.colL[k]);
+        put(P.colLc[k]);
         for (int32_t c : P.colComb[k]) put(c);
         put(P.colPot[k]);
+        // the chain is POTRF(k) -> TRSMc(k) -> L_diag(k+1) -> POTRF(k+1);
+        // L_diag(k+1) also waits for Md(k+1) (the diagonal tile's near
+        // pairs, inputs ready since TRSM(k-1)): ticket it before TRSMc(k)
+        // so it never holds up the chain (C4: it ended ~5 us after TRSMc)
+        if (md_early && k + 1 < T) put(P.colMd[k + 1]);
+        if (fuse) put(P.colTrsmC[k]);
         put(P.colLo[k]);
         if (fuse) put(P.colTrsm[k]);
         if (chain_first && fuse && k + 1 < T) {
             for (int32_t c : P.colChunk[k]) put(c);  // split-K pieces the next combines read
+            put(P.colMd[k + 1]);
             put(P.colM[k + 1]);
             put(P.colL[k + 1]);
+            put(P.colLc[k + 1]);
             for (int32_t c : P.colComb[k + 1]) put(c);
             put(P.colPot[k + 1]);
         }
+        if (k + D < T) put(P.colBd[k + D]);
         if (k + D < T) put(P.colB[k + D]);
+        if (k + 1 < T) put(P.colBd[k + 1]);
         if (k + 1 < T) put(P.colB[k + 1]);
+        if (k + 1 < T) put(P.colMd[k + 1]);
         if (k + 1 < T) put(P.colM[k + 1]);
+        put(P.colTrsmC[k]);
         put(P.colTrsm[k]);
         for (int32_t c : P.colChunk[k]) put(c);
     }
@@ -2028,7 +2169,7 @@ extern "C" int tc_plan_trace(tc_plan_t p, double* storage, void* stream, int64_t
     if (r) return r;
     for (int64_t t = 0; t < NT; ++t) task_launch[t] = p->ptasks[t].launch;
     for (int64_t i = 0; i < NL; ++i) {
-        launch_meta[3 * i] = p->launches[i].kind;
+        launch_meta[3 * i] = p->launches[i].kind | p->launches[i].tag;
         launch_meta[3 * i + 1] = p->launches[i].k;
         launch_meta[3 * i + 2] = p->launches[i].cls;
     }

@@ -1,0 +1,7 @@
+# Md(k+1) ticketed before TRSMc(k) (TC_MD_EARLY) x critical split: A/B, trace, parity subset
+mkdir -p gpurun_out/r3
+O=gpurun_out/r3
+bash tools/ab_env.sh "TC_MD_EARLY=0 TC_MD_EARLY=1 TC_CRIT=0" "c4:128 c3:128 c2:128"
+TC_DEBUG_ORDER=1 timeout 600 python tools/trace.py --workload c4 --tile 128 --ordering identity > $O/trace_c4_128_md.txt 2>&1; head -40 $O/trace_c4_128_md.txt; grep -A30 "launch timeline" $O/trace_c4_128_md.txt | tail -22; grep -i topolog $O/trace_c4_128_md.txt
+TC_DEBUG_ORDER=1 timeout 600 python tools/trace.py --workload c3 --tile 128 > $O/trace_c3_128_md.txt 2>&1; head -40 $O/trace_c3_128_md.txt | tail -28
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_stress.py -m gpu -x -q --timeout 300 > $O/pytest_md.log 2>&1; tail -2 $O/pytest_md.log
