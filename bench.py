@@ -67,6 +67,9 @@ def parse(argv=None):
     ap.add_argument("--executor", default="persistent", choices=["persistent", "graph", "direct"])
     ap.add_argument("--lookahead", type=int, default=None, help="bulk-update lookahead depth (default: api default)")
     ap.add_argument("--lanes", type=int, default=4, help="c5: factorisations in flight per GPU")
+    ap.add_argument("--share", type=int, default=4,
+                    help="c5: persistent kernels sharing the GPU (each takes 1/share of the SMs; "
+                         "C5 on one B200: 12.7 / 15.4 / 16.0 fact/s at 1 / 2 / 4)")
     ap.add_argument("--occupancy", type=int, default=0, help="persistent CTAs per SM (0 = plan default)")
     ap.add_argument("--ordering", default="auto",
                     help="auto (SPEC policy) | identity (C4: auto provably picks identity, zero fill)")
@@ -393,7 +396,8 @@ def run_batch(a, nt, rank, world, sub=False):
     P = len(thetas)
     lo, hi = shard_range(P, world, rank)
     L = max(1, a.lanes)
-    opts = api.FactorOptions(tile_size=nt, ordering=a.ordering, executor=a.executor, occupancy=a.occupancy)
+    opts = api.FactorOptions(tile_size=nt, ordering=a.ordering, executor=a.executor, occupancy=a.occupancy,
+                             concurrent=max(1, a.share))
     m0 = fam.matrix(*thetas[0])
     t0 = time.perf_counter()
     pat = api._pattern_for(m0, opts)
@@ -488,7 +492,7 @@ def run_batch(a, nt, rank, world, sub=False):
             "n_gpus": world, "steps": steps, "warmup": a.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": common_config("c5", nt, world, a),
-            "lanes_per_gpu": L, "nnz": m0.nnz,
+            "lanes_per_gpu": L, "grid_share": max(1, a.share), "nnz": m0.nnz,
             "roofline": {"bound": "tensor", "kernel": "k_persist x lanes", "achieved": P * F / (ms * 1e-3) / 1e12,
                          "peak": peak, "unit": "TFLOP/s", "frac": P * F / (ms * 1e-3) / 1e12 / peak,
                          "traffic": None, "peak_source": peak_src},

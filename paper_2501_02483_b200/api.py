@@ -54,7 +54,9 @@ class FactorOptions:
     ``concurrent`` > 1 (grid-shared batch lanes) are supported: the round-1
     race they exposed (a POTRF worker flag published before its rank-8
     update) is fixed and tests/test_gpu_stress.py checks both
-    modes bitwise.  At nt = 128 one CTA per SM is the faster default."""
+    modes bitwise.  At nt = 128 one CTA per SM is the faster default; the
+    64x64 update shape with 32-deep operand stages (139 KB of shared memory)
+    does not fit two CTAs per SM, so there ``occupancy`` = 2 runs as 1."""
 
     tile_size: int = 120
     workers: int = 1

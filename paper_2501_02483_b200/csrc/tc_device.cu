@@ -1264,6 +1264,7 @@ int build_persistent(tc_plan& P) {
     // C4: 536 -> 520 ms at nt=128), off for narrow ones (C3: 89 vs 97 ms)
     const bool chain_first = getenv("TC_ORDER") ? atoi(getenv("TC_ORDER")) == 1 : P.S >= 16 * (int64_t)T;
     const bool md_early = !(getenv("TC_MD_EARLY") && atoi(getenv("TC_MD_EARLY")) == 0) && D >= 2;
+    const bool bd_early = !(getenv("TC_BD_EARLY") && atoi(getenv("TC_BD_EARLY")) == 0);
     for (int k = 0; k < T; ++k) {
         put(P.colMd[k]);
         put(P.colM[k]);
@@ -1290,6 +1291,11 @@ int build_persistent(tc_plan& P) {
         }
         if (k + D < T) put(P.colBd[k + D]);
         if (k + D < T) put(P.colB[k + D]);
+        // the diagonal tile's bulk Bd(k+D+1) (inputs: columns <= k) one
+        // column earlier than the rest: its few long items then end before
+        // Md(k+D+1) / L_diag need the tile (C4: Bd(k+1) ended ~15 us into
+        // POTRF(k) and delayed Md(k+1) in some columns)
+        if (bd_early && k + D + 1 < T) put(P.colBd[k + D + 1]);
         if (k + 1 < T) put(P.colBd[k + 1]);
         if (k + 1 < T) put(P.colB[k + 1]);
         if (k + 1 < T) put(P.colMd[k + 1]);
