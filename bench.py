@@ -622,6 +622,30 @@ def run_ours(a, name, nt, rank, world):
         parity.update(device_backward_error(pat, m, storage, vals_dev, offs, sh))
         parity["tolerances"] = {"backward_error": 1e-12, "factor_rel_diff": 1e-12, "logdet_rel_diff": 1e-10}
 
+    # ---- triangular solves with the factor just computed:
+    # device sweep (plan.solve, one persistent launch per direction) for 1 and
+    # 8 right-hand sides, bytes = the factor's tiles read once per direction
+    solve_info = None
+    if not a.no_parity:
+        fbytes = storage.numel() * 8
+        solve_info = {"factor_bytes": int(fbytes), "hbm_peak_gbs": hbm_peak()[0]}
+        for nrhs in (1, 8):
+            rdev = torch.ones((nrhs, plan.T * nt), dtype=torch.float64, device="cuda")
+            plan.solve(storage, rdev, sh)
+            ts = []
+            for _ in range(5):
+                rdev.fill_(1.0)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                plan.solve(storage, rdev, sh)
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            ms_s = float(np.median(ts))
+            solve_info[f"nrhs{nrhs}"] = {"ms": ms_s, "gbs": 2 * fbytes / (ms_s * 1e-3) / 1e9,
+                                         "frac_hbm": 2 * fbytes / (ms_s * 1e-3) / 1e9 / solve_info["hbm_peak_gbs"]}
+            del rdev
+
     # ---- end to end through the public API (host values, H2D/D2H inside)
     e2e_ms = []
     del_vals = vals_dev
@@ -691,6 +715,8 @@ def run_ours(a, name, nt, rank, world):
             "logdet": ld, "bitwise_reproducible": reproducible}
     if parity is not None:
         line["parity"] = parity
+    if solve_info is not None:
+        line["solve"] = solve_info
     if prof:
         line["profile_direct"] = prof
     line["e2e"] = {"value": world * 1000.0 / e2e, "unit": "factorizations/s",
