@@ -1265,6 +1265,7 @@ int build_persistent(tc_plan& P) {
     const bool chain_first = getenv("TC_ORDER") ? atoi(getenv("TC_ORDER")) == 1 : P.S >= 16 * (int64_t)T;
     const bool md_early = !(getenv("TC_MD_EARLY") && atoi(getenv("TC_MD_EARLY")) == 0) && D >= 2;
     const bool bd_early = !(getenv("TC_BD_EARLY") && atoi(getenv("TC_BD_EARLY")) == 0);
+    const bool trsmr_late = getenv("TC_TRSMR_LATE") && atoi(getenv("TC_TRSMR_LATE")) == 1 && chain_first && fuse;
     for (int k = 0; k < T; ++k) {
         put(P.colMd[k]);
         put(P.colM[k]);
@@ -1279,18 +1280,27 @@ int build_persistent(tc_plan& P) {
         if (md_early && k + 1 < T) put(P.colMd[k + 1]);
         if (fuse) put(P.colTrsmC[k]);
         put(P.colLo[k]);
-        if (fuse) put(P.colTrsm[k]);
+        // TC_TRSMR_LATE=1: the non-critical TRSM(k) tiles, the L_crit(k+1)
+        // and split-K pieces that read them, ticketed behind B(k+D) (their
+        // CTAs then stream fewer of POTRF(k)'s panels in a spin); only on
+        // columns without reduced chains, whose combines the chain needs
+        const bool late = trsmr_late && k + 1 < T && P.colChunk[k].empty() && P.colComb[k + 1].empty();
+        if (fuse && !late) put(P.colTrsm[k]);
         if (chain_first && fuse && k + 1 < T) {
             for (int32_t c : P.colChunk[k]) put(c);  // split-K pieces the next combines read
             put(P.colMd[k + 1]);
             put(P.colM[k + 1]);
             put(P.colL[k + 1]);
-            put(P.colLc[k + 1]);
+            if (!late) put(P.colLc[k + 1]);
             for (int32_t c : P.colComb[k + 1]) put(c);
             put(P.colPot[k + 1]);
         }
         if (k + D < T) put(P.colBd[k + D]);
         if (k + D < T) put(P.colB[k + D]);
+        if (late) {
+            put(P.colTrsm[k]);
+            put(P.colLc[k + 1]);
+        }
         // the diagonal tile's bulk Bd(k+D+1) (inputs: columns <= k) one
         // column earlier than the rest: its few long items then end before
         // Md(k+D+1) / L_diag need the tile (C4: Bd(k+1) ended ~15 us into
